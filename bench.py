@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the batched syndrome BP decoder (arXiv 1711.01783 hot path).
+
+Workload (BASELINE.json configs[2], "C3"): stand-in rate-0.1 MET-LDPC code, n = 10^6
+(Table-1 counts exactly, R18), SNR 0.161, N = 100 iterations with per-frame
+syndrome early termination, 8-D MD reconciliation output as input.  One step = one
+pass of the whole hot path over one batch resident in HBM: LLRs from MD output
+(metldpc_llr_from_md) -> decode (metldpc_decode) -> FER counters (metldpc_batch_counters,
+NCCL all-reduce when N > 1).  Frames shard across ranks (frame f -> rank f mod G, weak
+scaling).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.  `value` = decoded Mb/s (n bits per frame, the paper's
+Table-1 convention) over all ranks, device-timed with CUDA events
+(max over ranks); `e2e` = the same through metldpc_decode_md_host from pinned host
+buffers (H2D + D2H inside the timed region); `roofline` = the check-node update phase
+(dominant kernel) against the measured HBM copy bandwidth; `cpu_baseline` = the CPU
+oracle (oracle/, fp32 replay M3) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "decoded info Mb/s (rate-0.1 n=1e6) at 1/2/4/8 B200; HBM GB/s vs peak"
+PAPER_MBPS = 30.39           # PAPER.md Table 1 (lines 69-72), rate 0.1, TITAN Xp, 64 codewords
+SUSTAINED_NOTE = "HBM peak = MEASURED_PEAKS.json hbm_gbs (STREAM-style copy, measured)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--family", default="r0.1")
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--snr", type=float, default=0.161)
+    ap.add_argument("--iters", type=int, default=100)
+    ap.add_argument("--frames", type=int, default=256, help="frames per GPU per step")
+    ap.add_argument("--distinct", type=int, default=64, help="distinct frames generated per rank (tiled)")
+    ap.add_argument("--rule", choices=["exact", "lut"], default="exact")
+    ap.add_argument("--no-et", action="store_true")
+    ap.add_argument("--lanes", type=int, default=64)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle work for cpu_baseline")
+    ap.add_argument("--data-key", type=int, default=0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- inputs
+
+def _gen_one(args):
+    family, n, snr, key, fid = args
+    from synth.codes import make_met_code
+    from synth.frames import gen_frame
+    code = make_met_code(family, n)
+    f = gen_frame(code, snr, key, fid)
+    return f["v"], f["xnorm"], f["synd"]
+
+
+def gen_frames(a, frame_ids):
+    from multiprocessing import get_context
+    jobs = [(a.family, a.n, a.snr, a.data_key, int(f)) for f in frame_ids]
+    procs = max(1, min(len(jobs), (os.cpu_count() or 4) // 2, 32))
+    with get_context("fork").Pool(procs) as pool:
+        out = pool.map(_gen_one, jobs)
+    return (np.stack([o[0] for o in out]), np.stack([o[1] for o in out]), np.stack([o[2] for o in out]))
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------------------- CPU oracle (baseline / reference)
+
+def oracle_throughput(a, code, v, xn, synd, budget_s: float, threads: int | None = None) -> dict:
+    """The oracle M3 (fp32 replay, as it stands) decoding frames on host threads, one frame
+    per thread.  Bounded sample: T frames x I iterations (I <= N) so it costs ~budget_s;
+    throughput is normalised to the workload's N iterations per frame."""
+    from oracle import bp
+    T = threads or max(1, min(host_cores(), 32, len(v)))
+    lam = [bp.llr_from_md_f32(v[i % len(v)], xn[i % len(v)], a.snr) for i in range(T)]
+    t0 = time.perf_counter()
+    bp.decode(code, lam[0], synd[0], 1, early_term=not a.no_et, rule=_rule(a), prec=32)
+    t_iter = max(time.perf_counter() - t0, 1e-3)
+    I = int(max(1, min(a.iters, budget_s / t_iter)))
+
+    def one(i):
+        return bp.decode(code, lam[i], synd[i % len(synd)], I, early_term=not a.no_et, rule=_rule(a), prec=32)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(T) as ex:
+        res = list(ex.map(one, range(T)))
+    dt = time.perf_counter() - t0
+    iters_done = sum(r["iters"] for r in res)
+    bits = T * code.n * (iters_done / T) / a.iters        # frames-equivalent at N iterations
+    return {"value": bits / dt / 1e6, "unit": "Mb/s", "cores": T, "kind": "oracle",
+            "sample": f"{T} frames (one per host thread) x {I} of N={a.iters} iterations, oracle M3 (fp32 replay, "
+                      f"oracle/bp_oracle.c) on n={code.n}; throughput normalised to N iterations/frame; "
+                      f"{dt:.1f} s wall"}
+
+
+def _rule(a):
+    return 0 if a.rule == "exact" else 1
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    def __init__(self, gpu_index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.f.flush()
+        rows = [r.split(",") for r in Path(self.f.name).read_text().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows if len(r) >= 9 for k in range(4) if r[5 + k].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- main
+
+def measured_peak_gbs() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def workload_name(a) -> str:
+    return (f"C3: MET-LDPC {a.family} stand-in n={a.n}, SNR {a.snr}, max {a.iters} iterations "
+            f"{'fixed' if a.no_et else 'with per-frame syndrome early termination'}, "
+            f"{a.frames} frames/GPU per step, 8-D MD LLR input")
+
+
+def run_reference(a, rank: int, world: int):
+    if rank != 0:
+        return
+    from synth.codes import make_met_code
+    code = make_met_code(a.family, a.n)
+    v, xn, synd = gen_frames(a, range(min(a.distinct, 32)))
+    T = max(1, min(host_cores(), 32))
+    budget = max(2.0, 150.0 / max(1, a.steps + a.warmup))
+    for _ in range(a.warmup):
+        oracle_throughput(a, code, v, xn, synd, budget, T)
+    vals, walls = [], []
+    last = None
+    for _ in range(a.steps):
+        t0 = time.perf_counter()
+        last = oracle_throughput(a, code, v, xn, synd, budget, T)
+        walls.append(time.perf_counter() - t0)
+        vals.append(last["value"])
+    value = statistics.mean(vals)
+    cpu = dict(last)
+    cpu["value"] = value
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "Mb/s", "n_gpus": a.gpus,
+           "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * statistics.mean(walls),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": value / PAPER_MBPS, "dtype": "f32",
+           "data": "synthetic", "config": {"workload": workload_name(a), "rule": a.rule.upper()},
+           "cpu_baseline": cpu,
+           "e2e": {"value": value, "unit": "Mb/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "gpu_launches": 0}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if a.impl == "reference":
+        return run_reference(a, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1711_01783_b200 import binding as B
+    from paper_1711_01783_b200 import metrics
+    from paper_1711_01783_b200.build import build
+    from synth.codes import make_met_code
+
+    if rank == 0:
+        build()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.barrier()
+        if rank != 0:
+            build()
+    dev = torch.device("cuda", local)
+    code = make_met_code(a.family, a.n)
+    st = code.stats()
+    F = a.frames
+    # frames of this rank: global ids f = rank + world * k; D distinct ones tiled to F
+    D = min(a.distinct, F)
+    ids = [rank + world * k for k in range(D)]
+    v_np, xn_np, sy_np = gen_frames(a, ids)
+    rep = (F + D - 1) // D
+    v = torch.from_numpy(np.tile(v_np, (rep, 1))[:F]).to(dev)
+    xn = torch.from_numpy(np.tile(xn_np, (rep, 1))[:F]).to(dev)
+    sy = torch.from_numpy(np.tile(sy_np, (rep, 1))[:F].view(np.int32)).to(dev)
+
+    hc = B.Code(code, device=local)
+    dec = B.Decoder(hc, F, rule=_rule(a), max_iter=a.iters, early_term=not a.no_et, lanes_per_group=a.lanes)
+    llr = torch.empty_like(v)
+    nw = (a.n + 31) // 32
+    bits = torch.empty((F, nw), dtype=torch.int32, device=dev)
+    iters = torch.empty(F, dtype=torch.int32, device=dev)
+    conv = torch.empty(F, dtype=torch.uint8, device=dev)
+    cnt = torch.zeros(4, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        dec.llr_from_md(v, xn, a.snr, out=llr)
+        dec.decode(llr, sy, out=(bits, iters, conv))
+        dec.counters(iters, conv, cnt)
+        if world > 1:
+            dist.all_reduce(cnt)
+
+    for _ in range(max(a.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    cnt.zero_()
+    dec.reset_profile()
+    dec.set_profiling(True)
+    launches0 = dec.profile()["launches"]
+    sampler = ClockSampler(local) if local == 0 or world == 1 else None
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0.record(stream)
+    for _ in range(a.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    dec.set_profiling(False)
+    prof = dec.profile()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    counters = cnt.cpu().numpy()   # all-reduced in-step when world > 1 (sum over ranks of K steps)
+    if world == 1:
+        pass
+    frames_total = F * world * a.steps
+    value = frames_total * a.n / (ms_max / 1e3) / 1e6
+
+    # ---- roofline of the dominant kernel (check-node update phase), live CUDA-event timing
+    bm = metrics.bytes_per_cw_iter(st["iter_edges"], st["n_deg1"], st["n_active"], st["m"])
+    peak, peak_src = measured_peak_gbs()
+    cn_gbs = prof["cn_lane_iters"] * bm["cn"] / (prof["cn_ms"] / 1e3) / 1e9 if prof["cn_ms"] > 0 else None
+    vn_lane_iters = prof["cn_lane_iters"]
+    vn_gbs = vn_lane_iters * bm["vn"] / (prof["vn_ms"] / 1e3) / 1e9 if prof["vn_ms"] > 0 else None
+    traffic = None
+    tpath = ROOT / "profiles" / "cn_traffic.json"
+    if tpath.exists():
+        try:
+            traffic = json.loads(tpath.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    it_bytes = F * world * a.steps * a.iters
+    roofline = {"bound": "hbm", "achieved": cn_gbs, "peak": peak, "unit": "GB/s",
+                "frac": (cn_gbs / peak) if cn_gbs else None, "traffic": traffic,
+                "kernel": "k_cn_update (all CN degree classes of one iteration)",
+                "bytes_per_launch": bm["cn"] * min(F, a.lanes), "peak_source": peak_src,
+                "avg_launch_ms": prof["cn_ms"] / max(1, prof["cn_launches"]),
+                "vn_update": {"achieved": vn_gbs, "frac": (vn_gbs / peak) if vn_gbs else None,
+                              "avg_launch_ms": prof["vn_ms"] / max(1, prof["vn_launches"])},
+                "iteration_alg_frac": (it_bytes * bm["alg"] / (ms_max / 1e3) / 1e9 / peak),
+                "iteration_two_pass_frac": (it_bytes * bm["two_pass"] / (ms_max / 1e3) / 1e9 / peak)}
+
+    # ---- e2e through the host-buffer C-ABI call (pinned host memory, copies inside)
+    e2e = None
+    if not a.no_e2e:
+        v_h = torch.from_numpy(np.tile(v_np, (rep, 1))[:F]).pin_memory()
+        xn_h = torch.from_numpy(np.tile(xn_np, (rep, 1))[:F]).pin_memory()
+        sy_h = torch.from_numpy(np.tile(sy_np, (rep, 1))[:F].view(np.int32)).pin_memory()
+        out_h = (torch.empty((F, nw), dtype=torch.int32).pin_memory(), torch.empty(F, dtype=torch.int32).pin_memory(),
+                 torch.empty(F, dtype=torch.uint8).pin_memory())
+        dec.decode_md_host(v_h, xn_h, sy_h, a.snr, out=out_h)      # warm (allocates staging)
+        if world > 1:
+            dist.barrier()
+        k_e2e = max(1, min(a.steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            dec.decode_md_host(v_h, xn_h, sy_h, a.snr, out=out_h)
+        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        W = (st["m"] + 31) // 32
+        e2e = {"value": F * world * k_e2e * a.n / float(dt.item()) / 1e6, "unit": "Mb/s",
+               "h2d_bytes_per_step": F * world * (a.n * 4 + (a.n // 8) * 4 + W * 4),
+               "d2h_bytes_per_step": F * world * (nw * 4 + 4 + 1),
+               "api": "metldpc_decode_md_host (pinned host buffers; H2D, LLR, decode, D2H per 64-lane group, "
+                      "copies overlapped with decode)", "steps": k_e2e}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = oracle_throughput(a, code, v_np, xn_np, sy_np, a.cpu_budget)
+
+    if rank == 0:
+        frames_c, conv_c, iters_c, bad_c = (int(x) for x in counters)
+        R = (a.n - st["m"]) / a.n
+        out = {
+            "metric": METRIC, "value": value, "unit": "Mb/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": value / PAPER_MBPS, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_name(a), "code": f"{a.family} stand-in (Table-1 counts), n={a.n}, "
+                       f"m={st['m']}, E={st['edges']}, E_it={st['iter_edges']}", "snr": a.snr,
+                       "beta": metrics.beta(R, a.snr), "max_iter": a.iters, "early_term": not a.no_et,
+                       "rule": a.rule.upper(), "frames_per_gpu": F, "distinct_frames_per_gpu": D,
+                       "lanes_per_group": a.lanes, "global_batch": F * world,
+                       "l2": "inputs larger than L2 (v 1 GB, edge messages 740 MB per 64-lane group)",
+                       "parallelism": f"dp{world} (frames sharded f mod G; NCCL all-reduce of FER counters)"},
+            "baseline_context": "vs_baseline = value / 30.39 Mb/s: paper Table 1 rate 0.1 on one TITAN Xp "
+                                "(64 codewords, fixed 100 iterations) -- context, other hardware",
+            "info_mbps": value * R, "fer": 1.0 - conv_c / max(1, frames_c), "mean_iters": iters_c / max(1, frames_c - bad_c),
+            "frames_timed": frames_c,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(prof["launches"] - launches0), "clocks": clocks,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,579 @@
+// decoder.cu -- C ABI of libmetldpc: code upload, decoder workspace, the batch
+// scheduler and the host-buffer end-to-end path.
+//
+// Schedule of one lane group (Figure 1 with per-frame early termination):
+//   scatter LLRs / syndromes -> init
+//   for l = 1..N:  CN update (tests iteration l-1 if ET) -> latch (ET) -> VN update
+//   syndrome test of iteration N -> final latch -> finalize (bits, iterations, flags)
+// Kernels early-exit once every lane of the group is latched.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "kernels.cuh"
+
+namespace metldpc {
+metldpc_status parse_alist(const char* path, int32_t* n_out, int32_t* m_out, std::vector<int64_t>* cn_ptr,
+                           std::vector<int32_t>* edge_vn, std::vector<int64_t>* vn_ptr,
+                           std::vector<int64_t>* vn_edge);
+}
+
+using namespace metldpc;
+
+#define CUDA_TRY(expr)                                                                        \
+    do {                                                                                      \
+        cudaError_t _e = (expr);                                                              \
+        if (_e != cudaSuccess)                                                                \
+            return fail(METLDPC_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));   \
+    } while (0)
+
+struct metldpc_decoder_s {
+    metldpc_code code = nullptr;
+    metldpc_config_t cfg{};
+    int32_t max_batch = 0;
+    int B = 64, C = 2;
+    struct ClassLaunch { int win; int32_t begin, count; int grid; };
+    std::vector<ClassLaunch> cn_classes;
+    int vn_grid = 0, chk_grid = 0;
+    // one group workspace
+    float *r = nullptr, *L = nullptr, *lam_a = nullptr, *lam1 = nullptr;
+    uint32_t *d1bits = nullptr, *synd_t = nullptr, *ctl = nullptr;  // ctl: act[4] unsat[4] invalid[4]
+    int32_t* iters = nullptr;
+    uint8_t* conv = nullptr;
+    int32_t* done = nullptr;
+    // host-path staging (2 slots of one group each)
+    float* st_llr[2] = {nullptr, nullptr};
+    uint32_t* st_synd[2] = {nullptr, nullptr};
+    uint32_t* st_bits[2] = {nullptr, nullptr};
+    int32_t* st_iters[2] = {nullptr, nullptr};
+    uint8_t* st_conv[2] = {nullptr, nullptr};
+    float* st_xnorm[2] = {nullptr, nullptr};
+    cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+    // accounting
+    int profiling = 0;
+    metldpc_profile_t prof{};
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, size_t>> ev_pending;  // (0 = cn, 1 = vn), start index; stop = start + 1
+    size_t ev_used = 0;
+};
+
+namespace {
+
+template <class T>
+metldpc_status dalloc(T** p, size_t count) {
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        cudaGetLastError();
+        return fail(e == cudaErrorMemoryAllocation ? METLDPC_ENOMEM : METLDPC_ECUDA,
+                    std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    return METLDPC_OK;
+}
+
+template <class T>
+void dfree(T*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+CodeDev code_dev(const metldpc_code c, int rule) {
+    CodeDev cd;
+    cd.n = c->host.n;
+    cd.m = c->host.m;
+    cd.n_a = c->host.n_a;
+    cd.n_1 = c->host.n_1;
+    cd.E_it = c->host.E_it;
+    cd.cn_aptr = c->d_cn_aptr;
+    cd.cn_dptr = c->d_cn_dptr;
+    cd.a_vn = c->d_a_vn;
+    cd.vn_aptr = c->d_vn_aptr;
+    cd.vn_aedge = c->d_vn_aedge;
+    cd.vmap = c->d_vmap;
+    cd.phi = (rule == METLDPC_RULE_EXACT) ? c->d_phi_exact : c->d_phi_lut;
+    cd.phi_top = phi_top();
+    return cd;
+}
+
+Group group_of(metldpc_decoder d) {
+    Group g;
+    g.B = d->B;
+    g.C = d->C;
+    g.r = d->r;
+    g.L = d->L;
+    g.lam_a = d->lam_a;
+    g.lam1 = d->lam1;
+    g.d1bits = d->d1bits;
+    g.synd_t = d->synd_t;
+    g.act = d->ctl;
+    g.unsat = d->ctl + 4;
+    g.invalid = d->ctl + 8;
+    g.iters = d->iters;
+    g.conv = d->conv;
+    g.done = d->done;
+    return g;
+}
+
+template <class T>
+metldpc_status upload(T** dst, const std::vector<T>& src) {
+    metldpc_status s = dalloc(dst, src.size());
+    if (s) return s;
+    if (!src.empty()) CUDA_TRY(cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return METLDPC_OK;
+}
+
+metldpc_status check_device(int32_t device, int* num_sms) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return fail(METLDPC_EUNSUPPORTED, "no CUDA device available");
+    }
+    if (device < 0 || device >= count) return fail(METLDPC_EINVAL, "device index out of range");
+    cudaDeviceProp p;
+    CUDA_TRY(cudaGetDeviceProperties(&p, device));
+    if (p.major != 10) return fail(METLDPC_EUNSUPPORTED, std::string("built for sm_100a; device is ") + p.name);
+    *num_sms = p.multiProcessorCount;
+    return METLDPC_OK;
+}
+
+// Records a kernel-timing event pair when profiling (CUDA events on the launch stream).
+size_t ev_begin(metldpc_decoder d, int kind, cudaStream_t s) {
+    if (!d->profiling) return size_t(-1);
+    while (d->ev_used + 2 > d->ev_pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        d->ev_pool.push_back(e);
+    }
+    size_t i = d->ev_used;
+    d->ev_used += 2;
+    cudaEventRecord(d->ev_pool[i], s);
+    d->ev_pending.push_back({kind, i});
+    return i;
+}
+
+void ev_end(metldpc_decoder d, size_t i, cudaStream_t s) {
+    if (i == size_t(-1)) return;
+    cudaEventRecord(d->ev_pool[i + 1], s);
+}
+
+void ev_collect(metldpc_decoder d) {
+    if (d->ev_pending.empty()) return;
+    cudaEventSynchronize(d->ev_pool[d->ev_pending.back().second + 1]);
+    for (auto& pr : d->ev_pending) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, d->ev_pool[pr.second], d->ev_pool[pr.second + 1]);
+        (pr.first == 0 ? d->prof.cn_ms : d->prof.vn_ms) += ms;
+    }
+    d->ev_pending.clear();
+    d->ev_used = 0;
+}
+
+// One lane group of nb <= B frames; pointers already offset to the group's first frame.
+metldpc_status decode_group(metldpc_decoder d, const float* llr, const uint32_t* synd, int nb, int N,
+                            uint32_t* bits_out, int32_t* iters_out, uint8_t* conv_out, cudaStream_t s) {
+    const metldpc_code c = d->code;
+    const CodeDev cd = code_dev(c, d->cfg.rule);
+    const Group g = group_of(d);
+    const bool et = d->cfg.early_term != 0;
+    CUDA_TRY(cudaMemsetAsync(d->ctl + 8, 0, 4 * sizeof(uint32_t), s));
+    launch_scatter(cd, g, llr, nb, s);
+    launch_pack_syndrome(cd, g, synd, nb, s);
+    launch_init_ctl(g, nb, s);
+    d->prof.launches += 3;
+    for (int l = 1; l <= N; ++l) {
+        size_t e = ev_begin(d, 0, s);
+        for (const auto& k : d->cn_classes) {
+            launch_cn(cd, g, d->cfg.rule, k.win, c->d_cls_cn + k.begin, k.count, k.grid, l, et && l >= 2, s);
+            d->prof.launches++;
+        }
+        ev_end(d, e, s);
+        d->prof.cn_launches++;
+        d->prof.cn_lane_iters += nb;
+        if (et && l >= 2) {
+            launch_latch(g, l - 1, false, s);
+            d->prof.launches++;
+        }
+        e = ev_begin(d, 1, s);
+        launch_vn(cd, g, d->vn_grid, s);
+        ev_end(d, e, s);
+        d->prof.vn_launches++;
+        d->prof.launches++;
+    }
+    launch_check(cd, g, d->chk_grid, N, s);
+    launch_latch(g, N, true, s);
+    launch_finalize(cd, g, nb, bits_out, iters_out, conv_out, s);
+    d->prof.launches += 3;
+    CUDA_TRY(cudaGetLastError());
+    return METLDPC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+// ------------------------------------------------------------------ code
+
+metldpc_status metldpc_code_create(int32_t device, int32_t n, int32_t m, int64_t num_edges, const int64_t* cn_ptr,
+                                   const int32_t* edge_vn, const int64_t* vn_ptr, const int64_t* vn_edge,
+                                   metldpc_code* out) {
+    if (!out) return fail(METLDPC_EINVAL, "out is NULL");
+    *out = nullptr;
+    metldpc_code c = new (std::nothrow) metldpc_code_s();
+    if (!c) return fail(METLDPC_ENOMEM, "host allocation");
+    metldpc_status s = build_layout(n, m, num_edges, cn_ptr, edge_vn, vn_ptr, vn_edge, &c->host);
+    if (s == METLDPC_OK) s = check_device(device, &c->num_sms);
+    if (s) {
+        delete c;
+        return s;
+    }
+    c->device = device;
+    cudaSetDevice(device);
+    const HostLayout& L = c->host;
+    std::vector<float> te(kPhiBins * 4), tl(kPhiBins * 2);
+    phi_table_exact(te.data());
+    phi_table_lut(tl.data());
+    if ((s = upload(&c->d_cn_aptr, L.cn_aptr)) || (s = upload(&c->d_cn_dptr, L.cn_dptr)) ||
+        (s = upload(&c->d_a_vn, L.a_vn)) || (s = upload(&c->d_vn_aptr, L.vn_aptr)) ||
+        (s = upload(&c->d_vn_aedge, L.vn_aedge)) || (s = upload(&c->d_vmap, L.vmap)) ||
+        (s = upload(&c->d_cls_cn, L.cls_cn)) ||
+        (s = upload(&c->d_phi_exact, te)) || (s = upload(&c->d_phi_lut, tl))) {
+        metldpc_code_destroy(c);
+        return s;
+    }
+    *out = c;
+    return METLDPC_OK;
+}
+
+metldpc_status metldpc_code_load_alist(int32_t device, const char* path, metldpc_code* out) {
+    if (!path || !out) return fail(METLDPC_EINVAL, "NULL argument");
+    int32_t n = 0, m = 0;
+    std::vector<int64_t> cn_ptr, vn_ptr, vn_edge;
+    std::vector<int32_t> edge_vn;
+    metldpc_status s = parse_alist(path, &n, &m, &cn_ptr, &edge_vn, &vn_ptr, &vn_edge);
+    if (s) return s;
+    return metldpc_code_create(device, n, m, int64_t(edge_vn.size()), cn_ptr.data(), edge_vn.data(), vn_ptr.data(),
+                               vn_edge.data(), out);
+}
+
+metldpc_status metldpc_code_info(metldpc_code code, metldpc_code_info_t* out) {
+    if (!code || !out) return fail(METLDPC_EINVAL, "NULL argument");
+    fill_info(code->host, out);
+    return METLDPC_OK;
+}
+
+void metldpc_code_destroy(metldpc_code c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    dfree(c->d_cn_aptr);
+    dfree(c->d_cn_dptr);
+    dfree(c->d_a_vn);
+    dfree(c->d_vn_aptr);
+    dfree(c->d_vn_aedge);
+    dfree(c->d_vmap);
+    dfree(c->d_cls_cn);
+    dfree(c->d_phi_exact);
+    dfree(c->d_phi_lut);
+    delete c;
+}
+
+// ------------------------------------------------------------------ decoder
+
+void metldpc_config_default(metldpc_config_t* cfg) {
+    if (!cfg) return;
+    cfg->rule = METLDPC_RULE_EXACT;
+    cfg->max_iter = 100;
+    cfg->early_term = 1;
+    cfg->lanes_per_group = 64;
+}
+
+metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, const metldpc_config_t* cfg_in,
+                                      metldpc_decoder* out) {
+    if (!code || !out) return fail(METLDPC_EINVAL, "NULL argument");
+    *out = nullptr;
+    metldpc_config_t cfg;
+    metldpc_config_default(&cfg);
+    if (cfg_in) cfg = *cfg_in;
+    if (cfg.rule != METLDPC_RULE_EXACT && cfg.rule != METLDPC_RULE_PHI_LUT) return fail(METLDPC_EINVAL, "unknown rule");
+    if (cfg.max_iter < 1) return fail(METLDPC_EINVAL, "max_iter must be >= 1");
+    if (cfg.lanes_per_group != 32 && cfg.lanes_per_group != 64 && cfg.lanes_per_group != 128)
+        return fail(METLDPC_EINVAL, "lanes_per_group must be 32, 64 or 128");
+    if (max_batch < 1) return fail(METLDPC_EINVAL, "max_batch must be >= 1");
+    cudaSetDevice(code->device);
+    metldpc_decoder d = new (std::nothrow) metldpc_decoder_s();
+    if (!d) return fail(METLDPC_ENOMEM, "host allocation");
+    d->code = code;
+    d->cfg = cfg;
+    d->max_batch = max_batch;
+    d->B = cfg.lanes_per_group;
+    d->C = d->B / 32;
+    const HostLayout& L = code->host;
+    const size_t B = size_t(d->B), C = size_t(d->C);
+    metldpc_status s;
+    if ((s = dalloc(&d->r, size_t(L.E_it) * B)) || (s = dalloc(&d->L, size_t(L.n_a) * B)) ||
+        (s = dalloc(&d->lam_a, size_t(L.n_a) * B)) || (s = dalloc(&d->lam1, size_t(L.n_1) * B)) ||
+        (s = dalloc(&d->d1bits, 2 * size_t(L.n_1) * C)) || (s = dalloc(&d->synd_t, size_t(L.m) * C)) ||
+        (s = dalloc(&d->ctl, 16)) || (s = dalloc(&d->iters, B)) || (s = dalloc(&d->conv, B)) ||
+        (s = dalloc(&d->done, 1))) {
+        metldpc_decoder_destroy(d);
+        return s;
+    }
+    cudaMemset(d->d1bits, 0, 2 * size_t(L.n_1) * C * sizeof(uint32_t));
+    cudaMemset(d->ctl, 0, 16 * sizeof(uint32_t));
+    const int sms = code->num_sms;
+    for (const auto& k : L.classes) {
+        const int win = cn_window(k.dlo);
+        const long items = long(k.count) * d->C;
+        const long full = long(sms) * cn_blocks_per_sm(cfg.rule, win);
+        const long need = (items + 7) / 8;
+        d->cn_classes.push_back({win, k.begin, k.count, int(std::max(1L, std::min(full, need)))});
+    }
+    d->vn_grid = sms * vn_blocks_per_sm();
+    d->chk_grid = sms * 4;
+    *out = d;
+    return METLDPC_OK;
+}
+
+void metldpc_decoder_destroy(metldpc_decoder d) {
+    if (!d) return;
+    cudaSetDevice(d->code->device);
+    dfree(d->r);
+    dfree(d->L);
+    dfree(d->lam_a);
+    dfree(d->lam1);
+    dfree(d->d1bits);
+    dfree(d->synd_t);
+    dfree(d->ctl);
+    dfree(d->iters);
+    dfree(d->conv);
+    dfree(d->done);
+    for (int k = 0; k < 2; ++k) {
+        dfree(d->st_llr[k]);
+        dfree(d->st_synd[k]);
+        dfree(d->st_bits[k]);
+        dfree(d->st_iters[k]);
+        dfree(d->st_conv[k]);
+        dfree(d->st_xnorm[k]);
+    }
+    if (d->s_h2d) cudaStreamDestroy(d->s_h2d);
+    if (d->s_comp) cudaStreamDestroy(d->s_comp);
+    if (d->s_d2h) cudaStreamDestroy(d->s_d2h);
+    for (auto e : d->ev_pool) cudaEventDestroy(e);
+    delete d;
+}
+
+// ------------------------------------------------------------------ LLR from MD output
+
+metldpc_status metldpc_llr_from_md(metldpc_decoder d, int32_t batch, int32_t dim, float snr, const float* v,
+                                   const float* xnorm, float* llr_out, uintptr_t stream) {
+    if (!d) return fail(METLDPC_EINVAL, "NULL decoder");
+    const int n = d->code->host.n;
+    if (batch < 0 || batch > d->max_batch) return fail(METLDPC_EINVAL, "batch out of range");
+    if (dim != 1 && dim != 2 && dim != 4 && dim != 8) return fail(METLDPC_EINVAL, "d must be 1, 2, 4 or 8");
+    if (n % dim) return fail(METLDPC_EINVAL, "n must be divisible by d");
+    if (!(snr > 0.0f) || !std::isfinite(snr)) return fail(METLDPC_EINVAL, "snr must be finite and > 0");
+    if (batch == 0) return METLDPC_OK;
+    if (!v || !llr_out) return fail(METLDPC_EINVAL, "NULL buffer");
+    cudaSetDevice(d->code->device);
+    const double sd = double(snr);
+    const float c = float(2.0 * std::sqrt(sd * (1.0 + sd)));
+    launch_md_llr(int64_t(batch) * n, n, dim, c, v, xnorm, llr_out, reinterpret_cast<cudaStream_t>(stream));
+    d->prof.launches++;
+    CUDA_TRY(cudaGetLastError());
+    return METLDPC_OK;
+}
+
+// ------------------------------------------------------------------ decode
+
+metldpc_status metldpc_decode(metldpc_decoder d, int32_t batch, const float* llr, const uint32_t* syndrome,
+                              int32_t max_iter, uint32_t* bits_out, int32_t* iters_out, uint8_t* conv_out,
+                              uintptr_t stream) {
+    if (!d) return fail(METLDPC_EINVAL, "NULL decoder");
+    if (batch < 0 || batch > d->max_batch) return fail(METLDPC_EINVAL, "batch out of range [0, max_batch]");
+    if (max_iter < 0 || max_iter > d->cfg.max_iter) return fail(METLDPC_EINVAL, "max_iter out of range");
+    if (batch == 0) return METLDPC_OK;
+    if (!llr || !syndrome || !bits_out || !iters_out || !conv_out) return fail(METLDPC_EINVAL, "NULL buffer");
+    const int N = max_iter ? max_iter : d->cfg.max_iter;
+    cudaSetDevice(d->code->device);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const HostLayout& L = d->code->host;
+    const size_t W = size_t(L.m + 31) / 32, NW = size_t(L.n + 31) / 32;
+    for (int f0 = 0; f0 < batch; f0 += d->B) {
+        const int nb = std::min(d->B, batch - f0);
+        metldpc_status st = decode_group(d, llr + size_t(f0) * L.n, syndrome + size_t(f0) * W, nb, N,
+                                         bits_out + size_t(f0) * NW, iters_out + f0, conv_out + f0, s);
+        if (st) return st;
+    }
+    return METLDPC_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Host-buffer pipeline shared by metldpc_decode_host (LLR input) and
+// metldpc_decode_md_host (MD output input): double-buffered staging; the H2D of group
+// g+1 and the D2H of group g-1 run on their own streams while group g decodes.
+metldpc_status host_pipeline(metldpc_decoder d, int32_t batch, int md, int32_t dim, float snr, const float* in_h,
+                             const float* xnorm_h, const uint32_t* synd_h, int32_t max_iter, uint32_t* bits_h,
+                             int32_t* iters_h, uint8_t* conv_h) {
+    const int N = max_iter ? max_iter : d->cfg.max_iter;
+    cudaSetDevice(d->code->device);
+    const HostLayout& L = d->code->host;
+    const size_t n = size_t(L.n), W = size_t(L.m + 31) / 32, NW = size_t(L.n + 31) / 32, B = size_t(d->B);
+    const size_t nx = md ? n / size_t(dim) : 0;
+    metldpc_status st;
+    if (!d->s_comp) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&d->s_h2d, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&d->s_comp, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&d->s_d2h, cudaStreamNonBlocking));
+        for (int k = 0; k < 2; ++k)
+            if ((st = dalloc(&d->st_llr[k], B * n)) || (st = dalloc(&d->st_synd[k], B * W)) ||
+                (st = dalloc(&d->st_bits[k], B * NW)) || (st = dalloc(&d->st_iters[k], B)) ||
+                (st = dalloc(&d->st_conv[k], B)) || (st = dalloc(&d->st_xnorm[k], B * n)))
+                return st;
+    }
+    float c_md = 0.f;
+    if (md) {
+        const double sd = double(snr);
+        c_md = float(2.0 * std::sqrt(sd * (1.0 + sd)));
+    }
+    cudaEvent_t in_ready[2], out_ready[2], slot_free[2], out_free[2];
+    for (int k = 0; k < 2; ++k) {
+        cudaEventCreateWithFlags(&in_ready[k], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&out_ready[k], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&slot_free[k], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&out_free[k], cudaEventDisableTiming);
+        cudaEventRecord(slot_free[k], d->s_comp);
+        cudaEventRecord(out_free[k], d->s_d2h);
+    }
+    int gi = 0;
+    st = METLDPC_OK;
+    for (int f0 = 0; f0 < batch && st == METLDPC_OK; f0 += d->B, ++gi) {
+        const int k = gi & 1;
+        const int nb = std::min(d->B, batch - f0);
+        cudaStreamWaitEvent(d->s_h2d, slot_free[k], 0);
+        cudaMemcpyAsync(d->st_llr[k], in_h + size_t(f0) * n, size_t(nb) * n * sizeof(float), cudaMemcpyHostToDevice,
+                        d->s_h2d);
+        if (md && xnorm_h)
+            cudaMemcpyAsync(d->st_xnorm[k], xnorm_h + size_t(f0) * nx, size_t(nb) * nx * sizeof(float),
+                            cudaMemcpyHostToDevice, d->s_h2d);
+        cudaMemcpyAsync(d->st_synd[k], synd_h + size_t(f0) * W, size_t(nb) * W * sizeof(uint32_t),
+                        cudaMemcpyHostToDevice, d->s_h2d);
+        cudaEventRecord(in_ready[k], d->s_h2d);
+        cudaStreamWaitEvent(d->s_comp, in_ready[k], 0);
+        cudaStreamWaitEvent(d->s_comp, out_free[k], 0);
+        if (md) {   // LLRs in place over the staged v (metldpc_llr_from_md, R13)
+            launch_md_llr(int64_t(nb) * int64_t(n), int(n), dim, c_md, d->st_llr[k], xnorm_h ? d->st_xnorm[k] : nullptr,
+                          d->st_llr[k], d->s_comp);
+            d->prof.launches++;
+        }
+        st = decode_group(d, d->st_llr[k], d->st_synd[k], nb, N, d->st_bits[k], d->st_iters[k], d->st_conv[k],
+                          d->s_comp);
+        cudaEventRecord(slot_free[k], d->s_comp);
+        cudaEventRecord(out_ready[k], d->s_comp);
+        cudaStreamWaitEvent(d->s_d2h, out_ready[k], 0);
+        cudaMemcpyAsync(bits_h + size_t(f0) * NW, d->st_bits[k], size_t(nb) * NW * sizeof(uint32_t),
+                        cudaMemcpyDeviceToHost, d->s_d2h);
+        cudaMemcpyAsync(iters_h + f0, d->st_iters[k], size_t(nb) * sizeof(int32_t), cudaMemcpyDeviceToHost, d->s_d2h);
+        cudaMemcpyAsync(conv_h + f0, d->st_conv[k], size_t(nb), cudaMemcpyDeviceToHost, d->s_d2h);
+        cudaEventRecord(out_free[k], d->s_d2h);
+    }
+    cudaError_t e = cudaStreamSynchronize(d->s_d2h);
+    for (int k = 0; k < 2; ++k) {
+        cudaEventDestroy(in_ready[k]);
+        cudaEventDestroy(out_ready[k]);
+        cudaEventDestroy(slot_free[k]);
+        cudaEventDestroy(out_free[k]);
+    }
+    if (st) return st;
+    if (e != cudaSuccess) return fail(METLDPC_ECUDA, std::string("host pipeline: ") + cudaGetErrorString(e));
+    return METLDPC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+metldpc_status metldpc_decode_host(metldpc_decoder d, int32_t batch, const float* llr_h, const uint32_t* synd_h,
+                                   int32_t max_iter, uint32_t* bits_h, int32_t* iters_h, uint8_t* conv_h) {
+    if (!d) return fail(METLDPC_EINVAL, "NULL decoder");
+    if (batch < 0 || batch > d->max_batch) return fail(METLDPC_EINVAL, "batch out of range [0, max_batch]");
+    if (max_iter < 0 || max_iter > d->cfg.max_iter) return fail(METLDPC_EINVAL, "max_iter out of range");
+    if (batch == 0) return METLDPC_OK;
+    if (!llr_h || !synd_h || !bits_h || !iters_h || !conv_h) return fail(METLDPC_EINVAL, "NULL buffer");
+    return host_pipeline(d, batch, 0, 1, 0.f, llr_h, nullptr, synd_h, max_iter, bits_h, iters_h, conv_h);
+}
+
+metldpc_status metldpc_decode_md_host(metldpc_decoder d, int32_t batch, int32_t dim, float snr, const float* v_h,
+                                      const float* xnorm_h, const uint32_t* synd_h, int32_t max_iter,
+                                      uint32_t* bits_h, int32_t* iters_h, uint8_t* conv_h) {
+    if (!d) return fail(METLDPC_EINVAL, "NULL decoder");
+    if (batch < 0 || batch > d->max_batch) return fail(METLDPC_EINVAL, "batch out of range [0, max_batch]");
+    if (max_iter < 0 || max_iter > d->cfg.max_iter) return fail(METLDPC_EINVAL, "max_iter out of range");
+    if (dim != 1 && dim != 2 && dim != 4 && dim != 8) return fail(METLDPC_EINVAL, "d must be 1, 2, 4 or 8");
+    if (d->code->host.n % dim) return fail(METLDPC_EINVAL, "n must be divisible by d");
+    if (!(snr > 0.0f) || !std::isfinite(snr)) return fail(METLDPC_EINVAL, "snr must be finite and > 0");
+    if (batch == 0) return METLDPC_OK;
+    if (!v_h || !synd_h || !bits_h || !iters_h || !conv_h) return fail(METLDPC_EINVAL, "NULL buffer");
+    return host_pipeline(d, batch, 1, dim, snr, v_h, xnorm_h, synd_h, max_iter, bits_h, iters_h, conv_h);
+}
+
+metldpc_status metldpc_batch_counters(metldpc_decoder d, int32_t batch, const int32_t* iters, const uint8_t* conv,
+                                      int64_t* counters_out, uintptr_t stream) {
+    if (!d) return fail(METLDPC_EINVAL, "NULL decoder");
+    if (batch < 0) return fail(METLDPC_EINVAL, "batch < 0");
+    if (batch == 0) return METLDPC_OK;
+    if (!iters || !conv || !counters_out) return fail(METLDPC_EINVAL, "NULL buffer");
+    cudaSetDevice(d->code->device);
+    launch_counters(batch, iters, conv, counters_out, reinterpret_cast<cudaStream_t>(stream));
+    d->prof.launches++;
+    CUDA_TRY(cudaGetLastError());
+    return METLDPC_OK;
+}
+
+// ------------------------------------------------------------------ debug / accounting
+
+metldpc_status metldpc_debug_dump(metldpc_decoder d, int32_t lane, float* r_out, float* L_out) {
+    if (!d) return fail(METLDPC_EINVAL, "NULL decoder");
+    if (lane < 0 || lane >= d->B) return fail(METLDPC_EINVAL, "lane out of range");
+    cudaSetDevice(d->code->device);
+    CUDA_TRY(cudaDeviceSynchronize());
+    const HostLayout& L = d->code->host;
+    if (r_out && L.E_it)
+        CUDA_TRY(cudaMemcpy2D(r_out, sizeof(float), d->r + lane, size_t(d->B) * sizeof(float), sizeof(float),
+                              size_t(L.E_it), cudaMemcpyDeviceToHost));
+    if (L_out && L.n_a)
+        CUDA_TRY(cudaMemcpy2D(L_out, sizeof(float), d->L + lane, size_t(d->B) * sizeof(float), sizeof(float),
+                              size_t(L.n_a), cudaMemcpyDeviceToHost));
+    return METLDPC_OK;
+}
+
+metldpc_status metldpc_set_profiling(metldpc_decoder d, int32_t enable) {
+    if (!d) return fail(METLDPC_EINVAL, "NULL decoder");
+    d->profiling = enable ? 1 : 0;
+    return METLDPC_OK;
+}
+
+metldpc_status metldpc_get_profile(metldpc_decoder d, metldpc_profile_t* out) {
+    if (!d || !out) return fail(METLDPC_EINVAL, "NULL argument");
+    ev_collect(d);
+    *out = d->prof;
+    return METLDPC_OK;
+}
+
+metldpc_status metldpc_reset_profile(metldpc_decoder d) {
+    if (!d) return fail(METLDPC_EINVAL, "NULL decoder");
+    ev_collect(d);
+    d->prof = metldpc_profile_t{};
+    return METLDPC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,62 @@
+// kernels.cuh -- launch interface of the sm_100a kernels (private).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace metldpc {
+
+// Device state of the lane group being decoded.  Arrays are codeword-interleaved:
+// element (slot s, lane b) lives at s * B + b, B = lanes per group (32/64/128), so
+// a warp (32 consecutive lanes) touches one full 128-byte line per slot
+// ("when the number of simultaneously decoded codewords is an integer
+// multiple of 32, both of the variable nodes and check nodes memory access are
+// consecutive").  C = B / 32 lane chunks; bit vectors over lanes are uint32 per chunk.
+struct Group {
+    int B, C;
+    float* r;          // [E_it][B]   CN->VN messages r_ji of active edges (Eqs. 2-3)
+    float* L;          // [n_a][B]    posterior LLR of active VNs (Eq. 5)
+    float* lam_a;      // [n_a][B]    channel LLR of active VNs (Eq. 1)
+    float* lam1;       // [n_1][B]    channel LLR of degree-1 VNs, CSR slot order
+    uint32_t* d1bits;  // [2][n_1][C] hard bits of degree-1 VNs, by iteration parity
+    uint32_t* synd_t;  // [m][C]      S_B bits, lane-transposed
+    uint32_t* act;     // [C]  lanes still iterating
+    uint32_t* unsat;   // [C]  lanes with an unsatisfied check in the tested iteration
+    uint32_t* invalid; // [C]  lanes with a non-finite LLR
+    int32_t* iters;    // [B]
+    uint8_t* conv;     // [B]
+    int32_t* done;     // [1]  all lanes latched
+};
+
+struct CodeDev {
+    int32_t n, m, n_a, n_1;
+    int64_t E_it;
+    const int32_t* cn_aptr;
+    const int32_t* cn_dptr;
+    const int32_t* a_vn;
+    const int32_t* vn_aptr;
+    const int32_t* vn_aedge;
+    const int32_t* vmap;
+    const float* phi;      // table of the selected rule
+    float phi_top;
+};
+
+// returns the number of CTAs per SM the CN kernel reaches (for persistent grids)
+int cn_window(int dlo);                      // index of the degree window starting at dlo
+int cn_blocks_per_sm(int rule, int win);
+int vn_blocks_per_sm();
+
+void launch_scatter(const CodeDev& cd, const Group& g, const float* llr, int nb, cudaStream_t s);
+void launch_pack_syndrome(const CodeDev& cd, const Group& g, const uint32_t* synd, int nb, cudaStream_t s);
+void launch_init_ctl(const Group& g, int nb, cudaStream_t s);
+void launch_cn(const CodeDev& cd, const Group& g, int rule, int win, const int32_t* cls_cn, int count, int grid,
+               int l, bool check, cudaStream_t s);
+void launch_vn(const CodeDev& cd, const Group& g, int grid, cudaStream_t s);
+void launch_check(const CodeDev& cd, const Group& g, int grid, int l, cudaStream_t s);
+void launch_latch(const Group& g, int l, bool final_, cudaStream_t s);
+void launch_finalize(const CodeDev& cd, const Group& g, int nb, uint32_t* bits_out, int32_t* iters_out,
+                     uint8_t* conv_out, cudaStream_t s);
+void launch_counters(int batch, const int32_t* iters, const uint8_t* conv, int64_t* out, cudaStream_t s);
+void launch_md_llr(int64_t total, int n, int d, float c, const float* v, const float* xnorm, float* out,
+                   cudaStream_t s);
+
+}  // namespace metldpc

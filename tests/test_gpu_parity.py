@@ -1,0 +1,259 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE north_star): hard decisions, iteration counts
+and converged flags bit-exact against the fp32 replay M3; messages bit-exact
+against M3 every iteration, and M3 is within 1e-3 max(1,|LLR|) of a
+teacher-forced fp64 step (tests/test_oracle.py), so the GPU is too.
+Inputs are seeded synthetic frames from synth/ (never from the CUDA path).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import bp  # noqa: E402
+from paper_1711_01783_b200 import binding as B  # noqa: E402
+from synth.codes import from_dense, make_met_code, random_code, write_alist  # noqa: E402
+from synth.frames import gen_batch, pack_bits, unpack_bits  # noqa: E402
+
+RULES = [B.RULE_EXACT, B.RULE_PHI_LUT]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1711_01783_b200.build import build
+    build()
+
+
+def _frames(code, snrs, key=0):
+    """Batch with frames at several SNRs (mix of converging and failing frames)."""
+    parts = [gen_batch(code, s, key, range(i * 1000, i * 1000 + k)) | {"snr": np.full(k, s)}
+             for i, (s, k) in enumerate(snrs)]
+    out = {k: np.concatenate([p[k] for p in parts]) for k in ("u", "v", "xnorm", "synd", "snr")}
+    return out
+
+
+def _llr_oracle(fr):
+    return np.stack([bp.llr_from_md_f32(fr["v"][i], fr["xnorm"][i], fr["snr"][i]) for i in range(len(fr["v"]))])
+
+
+def _gpu_decode(code_h, llr, synd, rule, max_iter, et=True, lanes=64, max_batch=None):
+    dec = B.Decoder(code_h, max_batch or llr.shape[0], rule=rule, max_iter=max_iter, early_term=et,
+                    lanes_per_group=lanes)
+    bits, iters, conv = dec.decode(torch.from_numpy(llr).cuda(), torch.from_numpy(synd.view(np.int32)).cuda())
+    torch.cuda.synchronize()
+    return dec, bits.cpu().numpy().view(np.uint32), iters.cpu().numpy(), conv.cpu().numpy()
+
+
+def _assert_frame_equal(code, o, bits_row, it, cv, tag=""):
+    ob = bp.decode  # noqa
+    assert it == o["iters"], (tag, it, o["iters"])
+    assert bool(cv) == o["converged"], tag
+    assert np.array_equal(unpack_bits(bits_row, code.n), o["bits"]), tag
+
+
+@pytest.fixture(scope="module")
+def c1():
+    code = make_met_code("r0.1", 2048)
+    return code, B.Code(code)
+
+
+# ----------------------------------------------------------------------------- LLR init (a1)
+
+@pytest.mark.parametrize("with_norm", [True, False])
+def test_llr_from_md_bit_exact(c1, with_norm):
+    code, h = c1
+    fr = _frames(code, [(0.161, 3), (0.3, 2)])
+    dec = B.Decoder(h, 8)
+    v = torch.from_numpy(fr["v"]).cuda()
+    out = torch.empty_like(v)
+    xn = torch.from_numpy(fr["xnorm"]).cuda() if with_norm else None
+    for i in range(len(fr["v"])):
+        B.metldpc_llr_from_md(dec.h, 1, 8, float(fr["snr"][i]), v[i:i + 1], None if xn is None else xn[i:i + 1],
+                              out[i:i + 1])
+    got = out.cpu().numpy()
+    for i in range(len(fr["v"])):
+        ref = bp.llr_from_md_f32(fr["v"][i], fr["xnorm"][i] if with_norm else None, fr["snr"][i])
+        assert np.array_equal(got[i].view(np.uint32), ref.view(np.uint32))
+
+
+# ----------------------------------------------------------------------------- full decode vs M3
+
+@pytest.mark.parametrize("rule", RULES)
+def test_c1_bits_iters_flags_bit_exact(c1, rule):
+    """C1 (BASELINE configs[0]): n=2048 rate 0.1, SNR 0.161 (4 frames) plus frames at
+    0.2/0.3/0.5 so early termination fires at many different iterations."""
+    code, h = c1
+    fr = _frames(code, [(0.161, 4), (0.2, 4), (0.3, 4), (0.5, 4)])
+    llr = _llr_oracle(fr)
+    _, bits, iters, conv = _gpu_decode(h, llr, fr["synd"], rule, 100)
+    nconv = 0
+    for i in range(len(llr)):
+        o = bp.decode(code, llr[i], fr["synd"][i], 100, early_term=True, rule=rule, prec=32)
+        _assert_frame_equal(code, o, bits[i], iters[i], conv[i], f"frame {i}")
+        nconv += o["converged"]
+    assert 4 <= nconv < len(llr)      # both regimes exercised
+
+
+@pytest.mark.parametrize("rule", RULES)
+def test_c1_messages_every_iteration(c1, rule):
+    """r^l and L^l of every lane bit-identical to the oracle's trace for l = 1..N (ET off)."""
+    code, h = c1
+    fr = _frames(code, [(0.161, 2), (0.3, 2)])
+    llr = _llr_oracle(fr)
+    N = 40
+    traces = [bp.decode(code, llr[i], fr["synd"][i], N, early_term=False, rule=rule, prec=32, trace=True)
+              for i in range(len(llr))]
+    dec = B.Decoder(h, len(llr), rule=rule, max_iter=N, early_term=False)
+    L_t = torch.from_numpy(llr).cuda()
+    S_t = torch.from_numpy(fr["synd"].view(np.int32)).cuda()
+    for l in range(1, N + 1):
+        dec.decode(L_t, S_t, max_iter=l)
+        for i in range(len(llr)):
+            r, L = dec.dump(i)
+            assert np.array_equal(r.view(np.uint32), traces[i]["r_trace"][l - 1].view(np.uint32)), (l, i)
+            assert np.array_equal(L.view(np.uint32), traces[i]["L_trace"][l - 1].view(np.uint32)), (l, i)
+
+
+@pytest.mark.parametrize("et", [True, False])
+def test_batch_lane_and_group_invariance(c1, et):
+    """S:220 / R12: a frame's result does not depend on batch size, lane or group size."""
+    code, h = c1
+    fr = _frames(code, [(0.161, 30), (0.3, 40), (0.6, 30)])
+    llr = _llr_oracle(fr)
+    ref = None
+    for lanes in (32, 64, 128):
+        for order in ("fwd", "rev"):
+            idx = np.arange(len(llr)) if order == "fwd" else np.arange(len(llr))[::-1].copy()
+            _, bits, iters, conv = _gpu_decode(h, llr[idx], fr["synd"][idx], B.RULE_EXACT, 60, et=et, lanes=lanes)
+            inv = np.argsort(idx)
+            res = (bits[inv], iters[inv], conv[inv])
+            if ref is None:
+                ref = res
+            else:
+                for a, b in zip(ref, res):
+                    assert np.array_equal(a, b), (lanes, order)
+    # single-frame batches agree too
+    for i in (0, 45, 99):
+        _, bits, iters, conv = _gpu_decode(h, llr[i:i + 1], fr["synd"][i:i + 1], B.RULE_EXACT, 60, et=et)
+        assert np.array_equal(bits[0], ref[0][i]) and iters[0] == ref[1][i] and conv[0] == ref[2][i]
+
+
+def test_ragged_batch_max_batch_and_host_path(c1):
+    """Ragged lane counts (batch % 32 != 0), batch < max_batch, and decode_host (host
+    buffers, pipelined copies) give the device-path results."""
+    code, h = c1
+    fr = _frames(code, [(0.2, 37), (0.4, 40)])
+    llr = _llr_oracle(fr)
+    _, bits, iters, conv = _gpu_decode(h, llr, fr["synd"], B.RULE_PHI_LUT, 50, max_batch=200)
+    dec = B.Decoder(h, 200, rule=B.RULE_PHI_LUT, max_iter=50)
+    hb, hi, hc = dec.decode_host(np.ascontiguousarray(llr), np.ascontiguousarray(fr["synd"]))
+    assert np.array_equal(hb, bits) and np.array_equal(hi, iters) and np.array_equal(hc, conv)
+    for i in (0, 36, 76):
+        o = bp.decode(code, llr[i], fr["synd"][i], 50, rule=B.RULE_PHI_LUT, prec=32)
+        _assert_frame_equal(code, o, bits[i], iters[i], conv[i])
+
+
+def test_edge_cases(c1):
+    """Zero noise -> l = 1, c = u; non-finite LLR -> iterations -1 (R24) without
+    disturbing neighbours; max_iter = 1; empty batch."""
+    code, h = c1
+    fr = _frames(code, [(0.3, 4)])
+    llr = _llr_oracle(fr)
+    clean = ((1.0 - 2.0 * fr["u"][0]) * 8.0).astype(np.float32)
+    llr2 = np.stack([clean, llr[1], llr[2], llr[3]])
+    llr2[2, 77] = np.inf
+    _, bits, iters, conv = _gpu_decode(h, llr2, fr["synd"], B.RULE_EXACT, 100)
+    assert iters[0] == 1 and conv[0] == 1 and np.array_equal(unpack_bits(bits[0], code.n), fr["u"][0])
+    assert iters[2] == -1 and conv[2] == 0 and not bits[2].any()
+    for i in (1, 3):
+        o = bp.decode(code, llr2[i], fr["synd"][i], 100, prec=32)
+        _assert_frame_equal(code, o, bits[i], iters[i], conv[i])
+    _, bits, iters, conv = _gpu_decode(h, llr, fr["synd"], B.RULE_EXACT, 1)
+    for i in range(4):
+        o = bp.decode(code, llr[i], fr["synd"][i], 1, prec=32)
+        _assert_frame_equal(code, o, bits[i], iters[i], conv[i])
+    dec = B.Decoder(h, 4)
+    B.metldpc_decode(dec.h, 0, None, None, 0, None, None, None)   # empty batch is a no-op
+
+
+def test_generic_degree_paths_and_alist(tmp_path):
+    """Random codes exercising every CN-degree window (0-4, 5-8, 9-12, 13-16, 17-32),
+    loaded through alist, against the oracle."""
+    rng = np.random.default_rng(21)
+    for t, (n, m, deg) in enumerate([(60, 20, (2, 3)), (80, 12, (2, 4)), (120, 10, (2, 4)), (200, 8, (2, 3))]):
+        code = random_code(n, m, rng, frac_deg1=0.3, act_deg=deg)
+        p = tmp_path / f"c{t}.alist"
+        write_alist(code, p)
+        h = B.Code(alist=str(p))
+        assert h.info.edges == code.num_edges and h.info.max_cn_deg == code.cn_degree.max()
+        u = rng.integers(0, 2, n).astype(np.uint8)
+        s = (code.dense().astype(int) @ u) % 2
+        llr = ((1 - 2.0 * u) * rng.uniform(0.2, 2.5, (8, n))).astype(np.float32)
+        llr[:, :5] *= -1
+        synd = np.stack([pack_bits(s)] * 8)
+        for rule in RULES:
+            _, bits, iters, conv = _gpu_decode(h, llr, synd, rule, 30)
+            for i in range(8):
+                o = bp.decode(code, llr[i], synd[i], 30, rule=rule, prec=32)
+                _assert_frame_equal(code, o, bits[i], iters[i], conv[i], f"code {t} frame {i}")
+
+
+def test_empty_check_row():
+    """A degree-0 CN with S_B bit 1 can never be satisfied (R23)."""
+    h = np.array([[1, 1, 0, 0], [0, 1, 1, 1], [0, 0, 0, 0]], np.uint8)
+    code = from_dense(h)
+    hd = B.Code(code)
+    llr = np.array([[2.0, 1.0, -1.5, 0.7]] * 2, np.float32)
+    synd = np.stack([pack_bits([0, 0, 0]), pack_bits([0, 0, 1])])
+    _, bits, iters, conv = _gpu_decode(hd, llr, synd, B.RULE_EXACT, 10)
+    for i in range(2):
+        o = bp.decode(code, llr[i], synd[i], 10, prec=32)
+        _assert_frame_equal(code, o, bits[i], iters[i], conv[i])
+    assert conv[1] == 0
+
+
+# ----------------------------------------------------------------------------- larger configs
+
+def test_c2_sampled_lanes():
+    """C2 (configs[1]): n=65,536, 64-codeword batch at SNR 0.161 + 0.2; lanes
+    0, 17, 38, 63 replayed by the oracle bit-exactly; every converged lane
+    satisfies H c = S_B."""
+    code = make_met_code("r0.1", 65536)
+    h = B.Code(code)
+    fr = _frames(code, [(0.161, 40), (0.2, 24)])
+    llr = _llr_oracle(fr)
+    _, bits, iters, conv = _gpu_decode(h, llr, fr["synd"], B.RULE_EXACT, 100)
+    for i in (0, 17, 38, 63):
+        o = bp.decode(code, llr[i], fr["synd"][i], 100, prec=32)
+        _assert_frame_equal(code, o, bits[i], iters[i], conv[i], f"lane {i}")
+    for i in np.flatnonzero(conv):
+        s = unpack_bits(fr["synd"][i], code.m)
+        assert np.array_equal(bp.syndrome(code, unpack_bits(bits[i], code.n)), s)
+
+
+@pytest.mark.parametrize("rule", RULES)
+def test_c3_full_size_sampled_lane(rule):
+    """C3 at BASELINE's full size (n = 10^6, rate 0.1, SNR 0.161, N = 100) in the bench's
+    launch configuration (64-lane groups, two groups): two sampled lanes (one per group)
+    replayed by the oracle bit-exactly."""
+    code = make_met_code("r0.1", 10 ** 6)
+    h = B.Code(code)
+    nf = 72
+    fr = gen_batch(code, 0.161, 0, range(nf))
+    dec = B.Decoder(h, nf, rule=rule, max_iter=100)
+    v = torch.from_numpy(fr["v"]).cuda()
+    xn = torch.from_numpy(fr["xnorm"]).cuda()
+    llr_d = dec.llr_from_md(v, xn, 0.161)
+    bits, iters, conv = dec.decode(llr_d, torch.from_numpy(fr["synd"].view(np.int32)).cuda())
+    bits = bits.cpu().numpy().view(np.uint32)
+    iters = iters.cpu().numpy()
+    conv = conv.cpu().numpy()
+    for i in (5, 70):
+        lam = bp.llr_from_md_f32(fr["v"][i], fr["xnorm"][i], 0.161)
+        o = bp.decode(code, lam, fr["synd"][i], 100, rule=rule, prec=32)
+        _assert_frame_equal(code, o, bits[i], iters[i], conv[i], f"lane {i}")
+    assert (iters > 0).all()
