@@ -198,8 +198,9 @@ metldpc_status metldpc_batch_counters(metldpc_decoder dec, int32_t batch, const 
 metldpc_status metldpc_debug_dump(metldpc_decoder dec, int32_t lane, float* r_out, float* L_out);
 
 /* The fp32 phi table of a rule (N2), host computed, no GPU touched:
- * EXACT 1600 x 4 floats (c0..c3 per bin), PHI_LUT 1600 x 2 floats (c0, c1), then one
- * trailing float PHI_TOP.  Returns the number of floats needed; writes if cap allows. */
+ * EXACT 800 x 4 floats (c0..c3 per bin, 16 bins per binade), PHI_LUT 1600 x 2 floats
+ * (c0, c1, 32 bins per binade), then one trailing float PHI_TOP.  Returns the number of
+ * floats needed; writes if cap allows. */
 int32_t metldpc_phi_table(int32_t rule, float* out, int32_t cap);
 
 /* Profiling: when enabled, CN/VN launches are bracketed by CUDA events on the

@@ -41,8 +41,12 @@
 #define R_MAX 30.0
 #define PHI_E_LO (-44)
 #define PHI_E_HI 6
-#define PHI_J 5
-#define PHI_NBIN (((PHI_E_HI) - (PHI_E_LO)) << PHI_J)
+/* bins per binade 2^J: EXACT J = 4 (cubic), PHI_LUT J = 5 (linear) -- DESIGN.md N2 */
+#define PHI_J_EXACT 4
+#define PHI_J_LUT 5
+#define PHI_NBIN_MAX (((PHI_E_HI) - (PHI_E_LO)) << PHI_J_LUT)
+static int phi_j(int rule) { return rule == 0 ? PHI_J_EXACT : PHI_J_LUT; }
+static int phi_nbin(int rule) { return ((PHI_E_HI) - (PHI_E_LO)) << phi_j(rule); }
 
 enum { RULE_EXACT = 0, RULE_PHI_LUT = 1 };
 
@@ -57,15 +61,15 @@ double orc_phi_def(double y) {
 /* phi'(y) = -1/sinh(y) */
 static double dphi_def(double y) { return -1.0 / sinh(y); }
 
-/* Bin b covers [y0, y0 + h): y0 = 2^e (1 + j/32), h = 2^e/32, e = -44 + b/32, j = b%32. */
-static void bin_knots(int b, double* y0, double* h) {
-    int e = PHI_E_LO + (b >> PHI_J);
-    int j = b & ((1 << PHI_J) - 1);
-    *y0 = ldexp(1.0 + (double)j / (double)(1 << PHI_J), e);
-    *h = ldexp(1.0, e - PHI_J);
+/* Bin b covers [y0, y0 + h): y0 = 2^e (1 + j/2^J), h = 2^(e-J), e = -44 + (b >> J), j = b mod 2^J. */
+static void bin_knots(int J, int b, double* y0, double* h) {
+    int e = PHI_E_LO + (b >> J);
+    int j = b & ((1 << J) - 1);
+    *y0 = ldexp(1.0 + (double)j / (double)(1 << J), e);
+    *h = ldexp(1.0, e - J);
 }
 
-/* DESIGN.md N2: the fp32 phi table of each rule.
+/* DESIGN.md N2: the fp32 phi table of each rule (EXACT 800 bins, PHI_LUT 1600 bins).
  *   EXACT  : 4 floats per bin, cubic Hermite on t in [0,1):
  *            c0 = f0, c1 = m0, c2 = 3(f1-f0) - 2 m0 - m1, c3 = 2(f0-f1) + m0 + m1,
  *            f = phi(knot), m = h * phi'(knot), evaluated in double, rounded.
@@ -73,11 +77,11 @@ static void bin_knots(int b, double* y0, double* h) {
  * Returns the number of floats written (cap permitting). */
 int orc_phi_table(int rule, float* out, int cap) {
     int per = (rule == RULE_EXACT) ? 4 : 2;
-    int need = PHI_NBIN * per;
+    int need = phi_nbin(rule) * per;
     if (!out || cap < need) return need;
-    for (int b = 0; b < PHI_NBIN; ++b) {
+    for (int b = 0; b < phi_nbin(rule); ++b) {
         double y0, h;
-        bin_knots(b, &y0, &h);
+        bin_knots(phi_j(rule), b, &y0, &h);
         double y1 = y0 + h;
         double f0 = orc_phi_def(y0), f1 = orc_phi_def(y1);
         if (rule == RULE_EXACT) {
@@ -96,15 +100,15 @@ int orc_phi_table(int rule, float* out, int cap) {
     return need;
 }
 
-static float g_tab[2][PHI_NBIN * 4];
+static float g_tab[2][PHI_NBIN_MAX * 4];
 static int g_tab_ready[2];
 static float g_phi_top;  /* phi(2^-44) rounded to fp32 */
 
 /* Builds both fp32 tables; the Python loader calls it once before any
  * (possibly multi-threaded) decode, so the lazy path below never races. */
 void orc_init(void) {
-    orc_phi_table(RULE_EXACT, g_tab[0], PHI_NBIN * 4);
-    orc_phi_table(RULE_PHI_LUT, g_tab[1], PHI_NBIN * 4);
+    orc_phi_table(RULE_EXACT, g_tab[0], PHI_NBIN_MAX * 4);
+    orc_phi_table(RULE_PHI_LUT, g_tab[1], PHI_NBIN_MAX * 4);
     g_phi_top = (float)orc_phi_def(ldexp(1.0, PHI_E_LO));
     g_tab_ready[0] = g_tab_ready[1] = 1;
 }
@@ -122,8 +126,9 @@ float orc_phi32(int rule, float y) {
     const uint32_t hi = (uint32_t)(127 + PHI_E_HI) << 23;
     if (bits < lo) return g_phi_top;
     if (bits >= hi) return 0.0f;
-    uint32_t idx = (bits - lo) >> (23 - PHI_J);
-    float t = (float)(bits & ((1u << (23 - PHI_J)) - 1u)) * (1.0f / (float)(1u << (23 - PHI_J)));
+    int J = phi_j(rule);
+    uint32_t idx = (bits - lo) >> (23 - J);
+    float t = (float)(bits & ((1u << (23 - J)) - 1u)) * (1.0f / (float)(1u << (23 - J)));
     if (rule == RULE_EXACT) {
         const float* c = &g_tab[0][4 * idx];
         return fmaf(fmaf(fmaf(c[3], t, c[2]), t, c[1]), t, c[0]);
@@ -141,12 +146,12 @@ double orc_phi64(int rule, double y) {
     int e;
     double mant = frexp(y, &e);          /* y = mant * 2^e, mant in [0.5, 1) */
     e -= 1;                               /* y = (2 mant) 2^e, 2 mant in [1, 2) */
-    double pos = (2.0 * mant - 1.0) * (double)(1 << PHI_J);
+    double pos = (2.0 * mant - 1.0) * (double)(1 << PHI_J_LUT);
     int j = (int)floor(pos);
     double t = pos - (double)j;
-    int b = ((e - PHI_E_LO) << PHI_J) + j;
+    int b = ((e - PHI_E_LO) << PHI_J_LUT) + j;
     double y0, h;
-    bin_knots(b, &y0, &h);
+    bin_knots(PHI_J_LUT, b, &y0, &h);
     double f0 = orc_phi_def(y0), f1 = orc_phi_def(y0 + h);
     return f0 + t * (f1 - f0);
 }

@@ -12,8 +12,11 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
+import os
+
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libmetldpc.so"
+# METLDPC_LIB selects an alternative in-tree build (kernel-variant experiments).
+LIB_PATH = Path(os.environ["METLDPC_LIB"]) if os.environ.get("METLDPC_LIB") else _PKG / "libmetldpc.so"
 
 OK, EINVAL, EFORMAT, ENOMEM, ECUDA, EUNSUPPORTED = range(6)
 RULE_EXACT, RULE_PHI_LUT = 0, 1

@@ -22,6 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 SOURCES = ["host_code.cpp", "kernels.cu", "decoder.cu"]
+EXTRA = os.environ.get("METLDPC_NVCC_EXTRA", "").split()
 HEADERS = ["internal.h", "kernels.cuh"]
 
 
@@ -29,7 +30,7 @@ def _cmd(src: Path, obj: Path) -> list[str]:
     if src.suffix == ".cpp":
         return ["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-Wall",
                 f"-I{INCLUDE}", "-c", str(src), "-o", str(obj)]
-    return [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xptxas", "-v",
+    return [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xptxas", "-v", *EXTRA,
             "-Xcompiler", "-fPIC,-ffp-contract=off", f"-I{INCLUDE}", "-c", str(src), "-o", str(obj)]
 
 

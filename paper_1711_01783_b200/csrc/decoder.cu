@@ -38,7 +38,7 @@ struct metldpc_decoder_s {
     metldpc_config_t cfg{};
     int32_t max_batch = 0;
     int B = 64, C = 2;
-    struct ClassLaunch { int win; int32_t begin, count; int grid; };
+    struct ClassLaunch { int D, nd; int32_t begin, count; int ts, grid; };
     std::vector<ClassLaunch> cn_classes;
     int vn_grid = 0, chk_grid = 0;
     // one group workspace
@@ -97,6 +97,7 @@ CodeDev code_dev(const metldpc_code c, int rule) {
     cd.vn_aptr = c->d_vn_aptr;
     cd.vn_aedge = c->d_vn_aedge;
     cd.vmap = c->d_vmap;
+    cd.cn_new = c->d_cn_new;
     cd.phi = (rule == METLDPC_RULE_EXACT) ? c->d_phi_exact : c->d_phi_lut;
     cd.phi_top = phi_top();
     return cd;
@@ -191,7 +192,7 @@ metldpc_status decode_group(metldpc_decoder d, const float* llr, const uint32_t*
     for (int l = 1; l <= N; ++l) {
         size_t e = ev_begin(d, 0, s);
         for (const auto& k : d->cn_classes) {
-            launch_cn(cd, g, d->cfg.rule, k.win, c->d_cls_cn + k.begin, k.count, k.grid, l, et && l >= 2, s);
+            launch_cn(cd, g, d->cfg.rule, k.D, k.nd, k.begin, k.count, k.ts, k.grid, l, et && l >= 2, s);
             d->prof.launches++;
         }
         ev_end(d, e, s);
@@ -237,13 +238,11 @@ metldpc_status metldpc_code_create(int32_t device, int32_t n, int32_t m, int64_t
     c->device = device;
     cudaSetDevice(device);
     const HostLayout& L = c->host;
-    std::vector<float> te(kPhiBins * 4), tl(kPhiBins * 2);
-    phi_table_exact(te.data());
-    phi_table_lut(tl.data());
+    const std::vector<float> te = phi_device_table(METLDPC_RULE_EXACT), tl = phi_device_table(METLDPC_RULE_PHI_LUT);
     if ((s = upload(&c->d_cn_aptr, L.cn_aptr)) || (s = upload(&c->d_cn_dptr, L.cn_dptr)) ||
         (s = upload(&c->d_a_vn, L.a_vn)) || (s = upload(&c->d_vn_aptr, L.vn_aptr)) ||
         (s = upload(&c->d_vn_aedge, L.vn_aedge)) || (s = upload(&c->d_vmap, L.vmap)) ||
-        (s = upload(&c->d_cls_cn, L.cls_cn)) ||
+        (s = upload(&c->d_cn_new, L.cn_new)) ||
         (s = upload(&c->d_phi_exact, te)) || (s = upload(&c->d_phi_lut, tl))) {
         metldpc_code_destroy(c);
         return s;
@@ -278,7 +277,7 @@ void metldpc_code_destroy(metldpc_code c) {
     dfree(c->d_vn_aptr);
     dfree(c->d_vn_aedge);
     dfree(c->d_vmap);
-    dfree(c->d_cls_cn);
+    dfree(c->d_cn_new);
     dfree(c->d_phi_exact);
     dfree(c->d_phi_lut);
     delete c;
@@ -306,6 +305,9 @@ metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, cons
     if (cfg.lanes_per_group != 32 && cfg.lanes_per_group != 64 && cfg.lanes_per_group != 128)
         return fail(METLDPC_EINVAL, "lanes_per_group must be 32, 64 or 128");
     if (max_batch < 1) return fail(METLDPC_EINVAL, "max_batch must be >= 1");
+    if ((code->host.E_it + 1) * int64_t(cfg.lanes_per_group) >= (int64_t(1) << 31) ||
+        (int64_t(code->host.n_a) + 1) * cfg.lanes_per_group >= (int64_t(1) << 31))
+        return fail(METLDPC_EUNSUPPORTED, "edge-message array exceeds 2^31 elements per lane group");
     cudaSetDevice(code->device);
     metldpc_decoder d = new (std::nothrow) metldpc_decoder_s();
     if (!d) return fail(METLDPC_ENOMEM, "host allocation");
@@ -329,11 +331,21 @@ metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, cons
     cudaMemset(d->ctl, 0, 16 * sizeof(uint32_t));
     const int sms = code->num_sms;
     for (const auto& k : L.classes) {
-        const int win = cn_window(k.dlo);
-        const long items = long(k.count) * d->C;
-        const long full = long(sms) * cn_blocks_per_sm(cfg.rule, win);
-        const long need = (items + 7) / 8;
-        d->cn_classes.push_back({win, k.begin, k.count, int(std::max(1L, std::min(full, need)))});
+        // The tiled kernels are specialised for 64-lane groups; other group sizes and the
+        // generic classes take the run-time-degree kernel.  Tile: up to cn_tile_max CNs per
+        // warp, fewer for small classes so every SM still gets >= 16 warp units.
+        const int D = (d->B == 64) ? k.D : -1;
+        const int warps_per_cta = kCnThreadsHost / 32;
+        int ts = 1;
+        long units = long(k.count) * d->C;
+        if (D >= 0) {
+            const long want = long(k.count) / (long(sms) * 16);
+            ts = int(std::max(1L, std::min(long(cn_tile_max(D, k.nd)), want)));
+            units = ((long(k.count) + ts - 1) / ts) * cn_units_per_tile(D, k.nd);
+        }
+        const long full = long(sms) * cn_blocks_per_sm(cfg.rule, D, k.nd);
+        const long need = (units + warps_per_cta - 1) / warps_per_cta;
+        d->cn_classes.push_back({D, k.nd, k.begin, k.count, ts, int(std::max(1L, std::min(full, need)))});
     }
     d->vn_grid = sms * vn_blocks_per_sm();
     d->chk_grid = sms * 4;
@@ -547,9 +559,12 @@ metldpc_status metldpc_debug_dump(metldpc_decoder d, int32_t lane, float* r_out,
     cudaSetDevice(d->code->device);
     CUDA_TRY(cudaDeviceSynchronize());
     const HostLayout& L = d->code->host;
-    if (r_out && L.E_it)
-        CUDA_TRY(cudaMemcpy2D(r_out, sizeof(float), d->r + lane, size_t(d->B) * sizeof(float), sizeof(float),
+    if (r_out && L.E_it) {   // device order (relabelled CNs) -> canonical active-edge CSR order
+        std::vector<float> tmp(size_t(L.E_it));
+        CUDA_TRY(cudaMemcpy2D(tmp.data(), sizeof(float), d->r + lane, size_t(d->B) * sizeof(float), sizeof(float),
                               size_t(L.E_it), cudaMemcpyDeviceToHost));
+        for (int64_t t = 0; t < L.E_it; ++t) r_out[L.perm_r[size_t(t)]] = tmp[size_t(t)];
+    }
     if (L_out && L.n_a)
         CUDA_TRY(cudaMemcpy2D(L_out, sizeof(float), d->L + lane, size_t(d->B) * sizeof(float), sizeof(float),
                               size_t(L.n_a), cudaMemcpyDeviceToHost));

@@ -83,32 +83,67 @@ metldpc_status build_layout(int32_t n, int32_t m, int64_t E, const int64_t* cn_p
     L = HostLayout();
     L.n = n; L.m = m; L.E = E;
     L.vmap.assign(n, 0);
-    int32_t n_a = 0, n_1 = 0;
+    int32_t n_a = 0;
     for (int32_t v = 0; v < n; ++v) {
         if (deg[v] >= 2) { L.vmap[v] = n_a++; L.act_vn.push_back(v); }
-        else L.vmap[v] = -1;  // fixed below once slots are known
         L.max_vn_deg = std::max(L.max_vn_deg, deg[v]);
     }
     L.n_a = n_a;
-    std::vector<int64_t> act_id(E, -1);
-    L.cn_aptr.assign(m + 1, 0);
-    L.cn_dptr.assign(m + 1, 0);
-    int64_t t = 0;
+    // canonical active-edge id: rank among active edges in the caller's CSR order
+    std::vector<int32_t> canon(E, -1);
+    int64_t tc = 0;
+    for (int64_t e = 0; e < E; ++e)
+        if (deg[edge_vn[e]] >= 2) canon[e] = int32_t(tc++);
+    // CN relabelling by degree class (stable): key 2D + nd for D <= 16, nd <= 1; else generic
+    std::vector<int32_t> cnd(m, 0);
     for (int32_t j = 0; j < m; ++j) {
-        L.cn_aptr[j] = int32_t(t);
-        L.cn_dptr[j] = n_1;
         int32_t d = int32_t(cn_ptr[j + 1] - cn_ptr[j]);
         if (d > kMaxCnDeg)
             return fail(METLDPC_EUNSUPPORTED, "CN " + std::to_string(j) + " has degree " + std::to_string(d) +
                                                   " > " + std::to_string(kMaxCnDeg));
-        L.max_cn_deg = std::max(L.max_cn_deg, d);
+        for (int64_t e = cn_ptr[j]; e < cn_ptr[j + 1]; ++e) cnd[j] += (deg[edge_vn[e]] == 1);
+    }
+    const int generic_key = 2 * (kMaxUnrolledCnDeg + 1);
+    auto cls_key = [&](int32_t j) {
+        const int d = int(cn_ptr[j + 1] - cn_ptr[j]);
+        return (d <= kMaxUnrolledCnDeg && cnd[j] <= 1) ? 2 * d + cnd[j] : generic_key;
+    };
+    std::vector<std::vector<int32_t>> buckets(generic_key + 1);
+    for (int32_t j = 0; j < m; ++j) buckets[cls_key(j)].push_back(j);
+    std::vector<int32_t> order;
+    order.reserve(m);
+    for (int key = 0; key <= generic_key; ++key) {
+        if (buckets[key].empty()) continue;
+        HostLayout::CnClass c{key < generic_key ? key / 2 : -1, key < generic_key ? key % 2 : -1,
+                              int32_t(order.size()), int32_t(buckets[key].size())};
+        order.insert(order.end(), buckets[key].begin(), buckets[key].end());
+        L.classes.push_back(c);
+    }
+    L.cn_new.assign(m, 0);
+    for (int32_t jn = 0; jn < m; ++jn) L.cn_new[order[jn]] = jn;
+    std::vector<int32_t> act_id(E, -1);
+    L.cn_aptr.assign(m + 1, 0);
+    L.cn_dptr.assign(m + 1, 0);
+    L.perm_r.reserve(size_t(tc));
+    int32_t t = 0, n_1 = 0;
+    for (int32_t jn = 0; jn < m; ++jn) {
+        const int32_t j = order[jn];
+        L.cn_aptr[jn] = t;
+        L.cn_dptr[jn] = n_1;
+        L.max_cn_deg = std::max(L.max_cn_deg, int32_t(cn_ptr[j + 1] - cn_ptr[j]));
         for (int64_t e = cn_ptr[j]; e < cn_ptr[j + 1]; ++e) {
             int32_t v = edge_vn[e];
-            if (deg[v] >= 2) { act_id[e] = t++; L.a_vn.push_back(L.vmap[v]); }
-            else { L.vmap[v] = ~n_1; n_1++; }
+            if (deg[v] >= 2) {
+                act_id[e] = t++;
+                L.a_vn.push_back(L.vmap[v]);
+                L.perm_r.push_back(canon[e]);
+            } else {
+                L.vmap[v] = ~n_1;
+                n_1++;
+            }
         }
     }
-    L.cn_aptr[m] = int32_t(t);
+    L.cn_aptr[m] = t;
     L.cn_dptr[m] = n_1;
     L.E_it = t;
     L.n_1 = n_1;
@@ -117,20 +152,9 @@ metldpc_status build_layout(int32_t n, int32_t m, int64_t E, const int64_t* cn_p
     for (int32_t a = 0; a < n_a; ++a) {
         int32_t v = L.act_vn[a];
         L.vn_aptr[a] = int32_t(L.vn_aedge.size());
-        for (int64_t k = vn_ptr[v]; k < vn_ptr[v + 1]; ++k) L.vn_aedge.push_back(int32_t(act_id[vn_edge[k]]));
+        for (int64_t k = vn_ptr[v]; k < vn_ptr[v + 1]; ++k) L.vn_aedge.push_back(act_id[vn_edge[k]]);
     }
     L.vn_aptr[n_a] = int32_t(L.vn_aedge.size());
-    L.cls_cn.clear();
-    L.cls_cn.reserve(m);
-    for (int w = 0; w < kNumCnWindows; ++w) {
-        HostLayout::CnClass c{kCnWinLo[w], kCnWinHi[w], int32_t(L.cls_cn.size()), 0};
-        for (int32_t j = 0; j < m; ++j) {
-            int32_t d = int32_t(cn_ptr[j + 1] - cn_ptr[j]);
-            if (d >= c.dlo && d <= c.dhi) L.cls_cn.push_back(j);
-        }
-        c.count = int32_t(L.cls_cn.size()) - c.begin;
-        if (c.count) L.classes.push_back(c);
-    }
     return METLDPC_OK;
 }
 
@@ -150,17 +174,17 @@ void fill_info(const HostLayout& L, metldpc_code_info_t* info) {
 static double phi_d(double y) { return std::log1p(2.0 / std::expm1(y)); }     // -ln tanh(y/2)
 static double dphi_d(double y) { return -1.0 / std::sinh(y); }
 
-static void knot(int b, double* y0, double* h) {
-    int e = kPhiELo + (b >> kPhiJ);
-    int j = b & ((1 << kPhiJ) - 1);
-    *y0 = std::ldexp(1.0 + double(j) / double(1 << kPhiJ), e);
-    *h = std::ldexp(1.0, e - kPhiJ);
+static void knot(int J, int b, double* y0, double* h) {
+    int e = kPhiELo + (b >> J);
+    int j = b & ((1 << J) - 1);
+    *y0 = std::ldexp(1.0 + double(j) / double(1 << J), e);
+    *h = std::ldexp(1.0, e - J);
 }
 
 void phi_table_exact(float* out) {
-    for (int b = 0; b < kPhiBins; ++b) {
+    for (int b = 0; b < kPhiBinsExact; ++b) {
         double y0, h;
-        knot(b, &y0, &h);
+        knot(kPhiJExact, b, &y0, &h);
         double y1 = y0 + h;
         double f0 = phi_d(y0), f1 = phi_d(y1);
         double m0 = h * dphi_d(y0), m1 = h * dphi_d(y1);
@@ -174,9 +198,9 @@ void phi_table_exact(float* out) {
 }
 
 void phi_table_lut(float* out) {
-    for (int b = 0; b < kPhiBins; ++b) {
+    for (int b = 0; b < kPhiBinsLut; ++b) {
         double y0, h;
-        knot(b, &y0, &h);
+        knot(kPhiJLut, b, &y0, &h);
         double f0 = phi_d(y0), f1 = phi_d(y0 + h);
         out[2 * b + 0] = float(f0);
         out[2 * b + 1] = float(f1 - f0);
@@ -184,6 +208,19 @@ void phi_table_lut(float* out) {
 }
 
 float phi_top() { return float(phi_d(std::ldexp(1.0, kPhiELo))); }
+
+std::vector<float> phi_device_table(int rule) {
+    const bool ex = (rule == METLDPC_RULE_EXACT);
+    const int nb = ex ? kPhiBinsExact : kPhiBinsLut, per = ex ? 4 : 2;
+    std::vector<float> base(size_t(nb) * per);
+    if (ex) phi_table_exact(base.data());
+    else phi_table_lut(base.data());
+    std::vector<float> dev(size_t(nb + 1) * kPhiCopies * per, 0.0f);   // last bin: zero sentinel
+    for (int b = 0; b < nb; ++b)
+        for (int k = 0; k < kPhiCopies; ++k)
+            for (int q = 0; q < per; ++q) dev[(size_t(b) * kPhiCopies + k) * per + q] = base[size_t(b) * per + q];
+    return dev;
+}
 
 // ------------------------------------------------------------------ alist
 
@@ -315,8 +352,7 @@ metldpc_status metldpc_code_check(int32_t n, int32_t m, int64_t num_edges, const
 }
 
 int32_t metldpc_phi_table(int32_t rule, float* out, int32_t cap) {
-    int32_t per = (rule == METLDPC_RULE_EXACT) ? 4 : 2;
-    int32_t need = kPhiBins * per + 1;
+    int32_t need = (rule == METLDPC_RULE_EXACT) ? kPhiBinsExact * 4 + 1 : kPhiBinsLut * 2 + 1;
     if (!out || cap < need) return need;
     if (rule == METLDPC_RULE_EXACT) phi_table_exact(out);
     else phi_table_lut(out);

@@ -10,18 +10,29 @@ namespace metldpc {
 
 constexpr int kMaxCnDeg = 32;          // templated CN kernel bound (metldpc.h: EUNSUPPORTED above)
 constexpr float kRMax = 30.0f;         // DESIGN.md R6
-constexpr int kPhiELo = -44, kPhiEHi = 6, kPhiJ = 5;
-constexpr int kPhiBins = (kPhiEHi - kPhiELo) << kPhiJ;      // 1600
-constexpr uint32_t kPhiLoBits = uint32_t(127 + kPhiELo) << 23;  // 2^-44
-constexpr uint32_t kPhiHiBits = uint32_t(127 + kPhiEHi) << 23;  // 2^6
+// phi tables (N2): 2^J bins per binade on [2^-44, 2^6); EXACT J = 4 (cubic,
+// 4 floats/bin), PHI_LUT J = 5 (linear, 2 floats/bin).
+constexpr int kPhiELo = -44, kPhiEHi = 6;
+constexpr int kPhiJExact = 4, kPhiJLut = 5;
+constexpr int kPhiBinsExact = (kPhiEHi - kPhiELo) << kPhiJExact;   // 800
+constexpr int kPhiBinsLut = (kPhiEHi - kPhiELo) << kPhiJLut;       // 1600
+constexpr uint32_t kPhiLoBits = uint32_t(127 + kPhiELo) << 23;     // 2^-44
+constexpr uint32_t kPhiHiBits = uint32_t(127 + kPhiEHi) << 23;     // 2^6
+// Device copy: each bin (plus one all-zero sentinel bin) replicated kPhiCopies times,
+// interleaved, so the 8 threads of a quarter-warp LDS phase read 8 distinct bank groups.
+constexpr int kPhiCopies = 8;
 
 void set_error(const std::string& msg);
 metldpc_status fail(metldpc_status s, const std::string& msg);
 
 // Host layout of H (DESIGN.md section 6 "Data layout").
+//   CN label        j' in [0, m): CNs relabelled so every degree class is one contiguous
+//                   range (classes by total degree D = 0..16, then one class for 17..32),
+//                   ascending original index within a class
 //   active VN index a in [0, n_a): VNs of degree >= 2, ascending original index
-//   active edge id  t in [0, E_it): CSR edges of active VNs, CSR order
-//   degree-1 slot   q in [0, n_1): CSR edges of degree-1 VNs, CSR order
+//   active edge id  t in [0, E_it): edges of active VNs, CN-major in j' order, CSR order
+//                   within a row (perm_r maps t to the canonical active-edge CSR order)
+//   degree-1 slot   q in [0, n_1): edges of degree-1 VNs, same order
 struct HostLayout {
     int32_t n = 0, m = 0;
     int64_t E = 0, E_it = 0;
@@ -33,17 +44,16 @@ struct HostLayout {
     std::vector<int32_t> vn_aedge;  // [E_it] active edge ids of active VN a, caller's CSC order
     std::vector<int32_t> vmap;      // [n] a (>= 0) for active VNs, ~q (< 0) for degree-1
     std::vector<int32_t> act_vn;    // [n_a] original VN id of active index
-    // CN degree classes: CNs grouped by total-degree window so each class kernel
-    // gets a register budget sized for its own degree (kernels.cu k_cn_update).
-    struct CnClass { int dlo, dhi; int32_t begin, count; };
+    std::vector<int32_t> cn_new;    // [m] original CN id -> j'
+    std::vector<int32_t> perm_r;    // [E_it] t -> canonical active-edge id
+    // CN degree classes: contiguous j' ranges with one total degree D <= 16 and nd <= 1
+    // degree-1 slots (a kernel instantiation per (D, nd), registers sized for it), or the
+    // generic class (D = -1: nd >= 2 or degree 17..32).
+    struct CnClass { int D, nd; int32_t begin, count; };
     std::vector<CnClass> classes;
-    std::vector<int32_t> cls_cn;    // [m] CN ids, grouped by class, ascending within a class
 };
 
-// Degree windows of the CN classes: [0,4] [5,8] [9,12] [13,16] unrolled; [17,32] generic.
-constexpr int kNumCnWindows = 5;
-constexpr int kCnWinLo[kNumCnWindows] = {0, 5, 9, 13, 17};
-constexpr int kCnWinHi[kNumCnWindows] = {4, 8, 12, 16, 32};
+constexpr int kMaxUnrolledCnDeg = 16;
 
 // Validates the edge-indexed CSR/CSC and builds the layout.  Returns OK/EFORMAT/EUNSUPPORTED.
 metldpc_status build_layout(int32_t n, int32_t m, int64_t E, const int64_t* cn_ptr,
@@ -53,8 +63,10 @@ metldpc_status build_layout(int32_t n, int32_t m, int64_t E, const int64_t* cn_p
 void fill_info(const HostLayout& L, metldpc_code_info_t* info);
 
 // fp32 phi tables (N2), generated here independently of the oracle.
-void phi_table_exact(float* out /*kPhiBins*4*/);
-void phi_table_lut(float* out /*kPhiBins*2*/);
+void phi_table_exact(float* out /*kPhiBinsExact*4*/);
+void phi_table_lut(float* out /*kPhiBinsLut*2*/);
+// replicated device layout [bin 0..nbins (sentinel)][copy][coefficients]
+std::vector<float> phi_device_table(int rule);
 float phi_top();
 
 }  // namespace metldpc
@@ -69,8 +81,8 @@ struct metldpc_code_s {
     int32_t* d_vn_aptr = nullptr;
     int32_t* d_vn_aedge = nullptr;
     int32_t* d_vmap = nullptr;
-    int32_t* d_cls_cn = nullptr;
-    float* d_phi_exact = nullptr;   // kPhiBins * 4
-    float* d_phi_lut = nullptr;     // kPhiBins * 2
+    int32_t* d_cn_new = nullptr;
+    float* d_phi_exact = nullptr;   // (kPhiBinsExact + 1) * 8 copies * 4
+    float* d_phi_lut = nullptr;     // (kPhiBinsLut + 1) * 8 copies * 2
     int num_sms = 148;
 };

@@ -23,23 +23,58 @@ namespace metldpc {
 
 // ------------------------------------------------------------------ phi (N2)
 
+// Device table layout: [bin 0..NB (zero sentinel)][copy 0..7][coefficients]; a thread
+// reads copy (lane & 7), so the 8 threads of an LDS phase hit 8 distinct bank groups
+// whatever their bins (no shared-memory bank conflicts, 1 wavefront per phase).
 template <int RULE>
-__device__ __forceinline__ float phi_dev(const float* __restrict__ tab, float y, float top) {
-    const uint32_t u = __float_as_uint(y);
-    const uint32_t uc = min(max(u, kPhiLoBits), kPhiHiBits - 1u);
-    const uint32_t idx = (uc - kPhiLoBits) >> (23 - kPhiJ);
-    const float t = __fmul_rn(__uint2float_rn(uc & ((1u << (23 - kPhiJ)) - 1u)), 1.0f / float(1u << (23 - kPhiJ)));
-    float v;
+struct PhiT;
+template <>
+struct PhiT<METLDPC_RULE_EXACT> {      // cubic Hermite, 16 bins per binade
+    static constexpr int J = kPhiJExact, ENTRY = 16, NB = kPhiBinsExact;
+    static constexpr int STRIDE = kPhiCopies * ENTRY;                        // bytes per bin
+    static constexpr int BIAS = int(kPhiLoBits >> (23 - J)) * STRIDE;       // bin(2^-44) * STRIDE
+    static constexpr int TAB_BYTES = (NB + 1) * STRIDE;
+};
+template <>
+struct PhiT<METLDPC_RULE_PHI_LUT> {    // linear, 32 bins per binade
+    static constexpr int J = kPhiJLut, ENTRY = 8, NB = kPhiBinsLut;
+    static constexpr int STRIDE = kPhiCopies * ENTRY;
+    static constexpr int BIAS = int(kPhiLoBits >> (23 - J)) * STRIDE;
+    static constexpr int TAB_BYTES = (NB + 1) * STRIDE;
+};
+
+// phi(y), y >= 0, exactly as DESIGN.md N2: clamping the bit pattern to [2^-44, 2^6]
+// reproduces both out-of-range rules with no selects (u = 2^-44: bin 0, t = 0, c0 =
+// (float)phi(2^-44) = PHI_TOP; u = 2^6: the zero sentinel bin, +0).  The bin's byte
+// offset is (u >> (23 - J)) * STRIDE = (u >> 12) with the low bits cleared, and
+// t = (u mod 2^(23-J)) / 2^(23-J) is formed exactly as (1 + m) - 1 from the mantissa bits.
+// tabk = table base + (lane & 7) * ENTRY - BIAS (see phi_tab_lane).
+template <int RULE>
+__device__ __forceinline__ float phi_dev(const char* tabk, float y) {
+    using P = PhiT<RULE>;
+    static_assert(P::STRIDE == (1 << (11 - P::J)), "(u >> (23 - J)) * STRIDE == (u & ~low) >> 12");
+    const uint32_t u = min(max(__float_as_uint(y), kPhiLoBits), kPhiHiBits);
+    const char* e = tabk + ((u & ~((1u << (23 - P::J)) - 1u)) >> 12);
+    const float t = __fsub_rn(__uint_as_float(((u << P::J) & 0x007FFFFFu) | 0x3F800000u), 1.0f);
     if constexpr (RULE == METLDPC_RULE_EXACT) {
-        const float4 c = reinterpret_cast<const float4*>(tab)[idx];
-        v = __fmaf_rn(__fmaf_rn(__fmaf_rn(c.w, t, c.z), t, c.y), t, c.x);
+        const float4 c = *reinterpret_cast<const float4*>(e);
+        return __fmaf_rn(__fmaf_rn(__fmaf_rn(c.w, t, c.z), t, c.y), t, c.x);
     } else {
-        const float2 c = reinterpret_cast<const float2*>(tab)[idx];
-        v = __fmaf_rn(c.y, t, c.x);
+        const float2 c = *reinterpret_cast<const float2*>(e);
+        return __fmaf_rn(c.y, t, c.x);
     }
-    v = (u < kPhiLoBits) ? top : v;
-    v = (u >= kPhiHiBits) ? 0.0f : v;
-    return v;
+}
+
+template <int RULE>
+__device__ __forceinline__ const char* phi_tab_lane(const char* smem, int lane) {
+    return smem + (lane & 7) * PhiT<RULE>::ENTRY - PhiT<RULE>::BIAS;
+}
+
+template <int RULE>
+__device__ __forceinline__ void load_phi_table(char* smem, const float* phi) {
+    using P = PhiT<RULE>;
+    for (int i = threadIdx.x; i < P::TAB_BYTES / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(smem)[i] = __ldg(reinterpret_cast<const uint4*>(phi) + i);
 }
 
 // ------------------------------------------------------------------ check-node update (a2 + a4)
@@ -50,118 +85,263 @@ struct CnCtl {
     int rpar, wpar;
 };
 
-// One CN j, one 32-lane chunk c, total degree d (active edges first, then degree-1):
-// DESIGN.md N1 in registers.  Eqs. (2)-(3), with the syndrome sign (R1).
-// FIXED: d == D known at compile time (fully unrolled, arrays in registers);
-// otherwise d <= D at run time (generic path for rare high-degree CNs).
-template <int RULE, int D, bool FIXED>
-__device__ __forceinline__ void cn_item(const CodeDev& cd, const Group& g, const float* tab, const CnCtl& k,
-                                        int j, int c, int lane, uint32_t amask, int ab, int na, int db, int d_rt,
-                                        uint32_t* s_unsat) {
-    const int d = FIXED ? D : d_rt;
-    const int B = g.B, C = g.C;
-    const size_t off = size_t(c) * 32 + lane;
-    const int sbit = (__ldg(g.synd_t + size_t(j) * C + c) >> lane) & 1;
-    if constexpr (FIXED && D == 0) {   // empty row: satisfied iff S_B[j] = 0
-        if (k.check) {
-            const uint32_t mm = __ballot_sync(FULL, sbit) & amask;
-            if (mm && lane == 0) atomicOr(&s_unsat[c], mm);
-        }
-        return;
-    } else {
-        const int idx = (lane < na) ? __ldg(cd.a_vn + ab + lane) : 0;
-        float p[D], P[D], lam1[D];
-        uint32_t negmask = 0;
-        int chk = sbit;
+constexpr int kCnThreads = 512;   // 2 CTAs x 16 warps per SM (the replicated table is 100 KB)
+
+// DESIGN.md N1 for one CN and one lane (fp32, slot order: actives, then the degree-1
+// slot): Eqs. (2)-(3) in sign/phi form with the syndrome sign (R1).
+// Returns the syndrome-test bit (N4) of iteration l-1; writes r for active slots and
+// the degree-1 decision bit.
+template <int RULE, int NA, int ND>
+__device__ __forceinline__ uint32_t cn_lane(const char* tabk, const float (&Lv)[NA > 0 ? NA : 1],
+                                            const float (&ro)[NA > 0 ? NA : 1], float lam, uint32_t sbit,
+                                            uint32_t d1prev, float* pr, bool act, uint32_t& d1bit) {
+    constexpr int D = NA + ND;
+    float p[D], P[D];
+    uint32_t xb[D];     // bits of x + 0.0f: sign bit = [x < 0] exactly (-0 + 0 = +0), N1 / R2
+    uint32_t par = sbit << 31;                            // bit 31: s_j XOR all n_k
+    uint32_t chk = sbit ^ d1prev;
 #pragma unroll
+    for (int s = 0; s < NA; ++s) {
+        const float x = __fsub_rn(Lv[s], ro[s]);         // extrinsic q = L - r (R10)
+        chk ^= uint32_t(Lv[s] < 0.0f);                    // c_v^{l-1} (a decision: comparison)
+        xb[s] = __float_as_uint(__fadd_rn(x, 0.0f));
+        par ^= xb[s];
+        p[s] = phi_dev<RULE>(tabk, fabsf(x));
+    }
+    if constexpr (ND > 0) {                               // degree-1 VN sends its prior
+        xb[NA] = __float_as_uint(__fadd_rn(lam, 0.0f));
+        par ^= xb[NA];
+        p[NA] = phi_dev<RULE>(tabk, fabsf(lam));
+    }
+    float acc = 0.0f;
+#pragma unroll
+    for (int s = 0; s < D; ++s) { P[s] = acc; acc = __fadd_rn(acc, p[s]); }
+    float Q = 0.0f;
+#pragma unroll
+    for (int s = D - 1; s >= 0; --s) {
+        const float S = __fadd_rn(P[s], Q);
+        const float mag = fminf(phi_dev<RULE>(tabk, S), kRMax);
+        const float o = __uint_as_float(__float_as_uint(mag) | ((par ^ xb[s]) & 0x80000000u));
+        if (s < NA) {
+            if (act) __stcs(pr + s * 64, o);
+        } else {
+            d1bit = uint32_t(__fadd_rn(lam, o) < 0.0f);   // Step 5 for VN_b
+        }
+        if (s > 0) Q = __fadd_rn(Q, p[s]);
+    }
+    return chk;
+}
+
+// Asynchronous L2 prefetch of a contiguous range by the TMA unit (no registers held).
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+#ifndef METLDPC_CN_PF
+#define METLDPC_CN_PF 4     // CNs of look-ahead for the r / lambda L2 prefetch
+#endif
+
+// One degree class (CN labels [begin, begin + count), NA active + ND <= 1 degree-1 slots)
+// for 64-lane groups.  Work unit = a tile of ts consecutive CNs owned by one warp; for
+// NA <= 4 the warp covers both 32-lane chunks (each thread: lanes `lane` and `lane + 32`,
+// two independent dependency chains), for larger NA one chunk per unit (register budget).
+// The tile's metadata is one coalesced load per array, its active-edge VN indices
+// (pre-scaled to row offsets) are staged in shared memory, and the r / lambda rows of
+// the CN PF positions ahead are prefetched into L2 by the TMA unit.
+template <int RULE, int NA, int ND>
+__global__ void __launch_bounds__(kCnThreads, 2) k_cn_tile(CodeDev cd, Group g, CnCtl k, int begin, int count,
+                                                           int ts) {
+    using PT = PhiT<RULE>;
+    constexpr int LPT = (NA <= 4) ? 2 : 1;     // lanes per thread
+    constexpr int UPT = 2 / LPT;               // units per tile
+    constexpr int NAS = NA > 0 ? NA : 1;
+    constexpr int STAGE = (NA <= 4 ? 32 : 8) * NAS;
+    extern __shared__ __align__(16) char smem[];
+    __shared__ uint32_t s_unsat[2], s_act[2];
+    if (*reinterpret_cast<volatile int*>(g.done)) return;
+    load_phi_table<RULE>(smem, cd.phi);
+    if (threadIdx.x < 2) { s_unsat[threadIdx.x] = 0u; s_act[threadIdx.x] = g.act[threadIdx.x]; }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const char* tabk = phi_tab_lane<RULE>(smem, lane);
+    int* s_idx = reinterpret_cast<int*>(smem + PT::TAB_BYTES) + warp * STAGE;
+    const uint32_t am0 = s_act[0], am1 = s_act[1];
+    const int wpb = blockDim.x >> 5;
+    const int ntiles = (count + ts - 1) / ts;
+    uint32_t un0 = 0, un1 = 0;
+    for (int u = blockIdx.x * wpb + warp; u < ntiles * UPT; u += gridDim.x * wpb) {
+        const int tile = u / UPT;
+        const int c0 = (UPT == 2) ? (u & 1) : 0;            // first chunk of this unit
+        const uint32_t amA = c0 ? am1 : am0;                  // mask of chunk c0
+        if ((LPT == 2 ? (am0 | am1) : amA) == 0u) continue;
+        const int j0 = begin + tile * ts;
+        const int nt = min(ts, begin + count - j0);
+        const bool on = lane < nt;
+        const int a_l = on ? __ldg(cd.cn_aptr + j0 + lane) : 0;
+        const int d_l = on ? __ldg(cd.cn_dptr + j0 + lane) : 0;
+        const uint2 sw_l = on ? __ldg(reinterpret_cast<const uint2*>(g.synd_t) + (j0 + lane)) : make_uint2(0, 0);
+        if constexpr (NA + ND == 0) {          // empty rows: satisfied iff S_B[j] = 0
+            for (int i = 0; i < nt; ++i) {
+                un0 |= __shfl_sync(FULL, sw_l.x, i);
+                un1 |= __shfl_sync(FULL, sw_l.y, i);
+            }
+            continue;
+        } else {
+            const int A0 = __shfl_sync(FULL, a_l, 0);
+            if constexpr (NA > 0) {
+                __syncwarp();
+                for (int e = lane; e < nt * NA; e += 32) s_idx[e] = __ldg(cd.a_vn + A0 + e) * 64;
+                __syncwarp();
+            }
+            if (lane < min(nt, METLDPC_CN_PF)) {    // look-ahead for the first CNs of the tile
+                if constexpr (NA > 0) prefetch_l2(g.r + size_t(a_l) * 64, NA * 256);
+                if constexpr (ND > 0) prefetch_l2(g.lam1 + size_t(d_l) * 64, 256);
+            }
+            for (int i = 0; i < nt; ++i) {
+                const int ab = __shfl_sync(FULL, a_l, i);
+                const int q0 = __shfl_sync(FULL, d_l, i);
+                const uint32_t swx = __shfl_sync(FULL, sw_l.x, i), swy = __shfl_sync(FULL, sw_l.y, i);
+                {
+                    const int ip = i + METLDPC_CN_PF;    // keep the DRAM stream PF CNs ahead
+                    const int abp = __shfl_sync(FULL, a_l, ip & 31), q0p = __shfl_sync(FULL, d_l, ip & 31);
+                    if (lane == 0 && ip < nt) {
+                        if constexpr (NA > 0) prefetch_l2(g.r + size_t(abp) * 64, NA * 256);
+                        if constexpr (ND > 0) prefetch_l2(g.lam1 + size_t(q0p) * 64, 256);
+                    }
+                }
+                const int* idx = s_idx + (ab - A0);
+                const float* pL = g.L + (c0 * 32 + lane);
+                float* pr = g.r + (size_t(ab) * 64 + c0 * 32 + lane);
+                float Lv[LPT][NAS], ro[LPT][NAS], lam[LPT];
+                uint32_t w[LPT];
+#pragma unroll
+                for (int s = 0; s < NA; ++s) {
+                    const int o = idx[s];
+#pragma unroll
+                    for (int h = 0; h < LPT; ++h) {
+                        Lv[h][s] = __ldg(pL + o + h * 32);
+                        ro[h][s] = k.first ? 0.0f : __ldcs(pr + s * 64 + h * 32);
+                    }
+                }
+                uint2 wv = make_uint2(0, 0);
+                if constexpr (ND > 0) {
+                    const float* pl = g.lam1 + (size_t(q0) * 64 + c0 * 32 + lane);
+#pragma unroll
+                    for (int h = 0; h < LPT; ++h) lam[h] = __ldcs(pl + h * 32);
+                    if (k.check) wv = __ldg(reinterpret_cast<const uint2*>(g.d1bits) + (size_t(k.rpar) * cd.n_1 + q0));
+                } else {
+#pragma unroll
+                    for (int h = 0; h < LPT; ++h) lam[h] = 0.0f;
+                }
+                uint32_t chk[LPT], b[LPT];
+#pragma unroll
+                for (int h = 0; h < LPT; ++h) {
+                    const int c = c0 + h;
+                    const uint32_t sbit = ((c ? swy : swx) >> lane) & 1u;
+                    w[h] = (((c ? wv.y : wv.x) >> lane) & 1u);
+                    const bool act = (((c ? am1 : am0) >> lane) & 1u) != 0u;
+                    b[h] = 0;
+                    chk[h] = cn_lane<RULE, NA, ND>(tabk, Lv[h], ro[h], lam[h], sbit, w[h], pr + h * 32, act, b[h]);
+                }
+#pragma unroll
+                for (int h = 0; h < LPT; ++h) {
+                    const uint32_t bal = __ballot_sync(FULL, chk[h]);
+                    if (c0 + h) un1 |= bal;
+                    else un0 |= bal;
+                }
+                if constexpr (ND > 0) {
+                    uint32_t bal[LPT];
+#pragma unroll
+                    for (int h = 0; h < LPT; ++h) bal[h] = __ballot_sync(FULL, b[h]);
+                    if (lane == 0) {
+                        uint32_t* wp = g.d1bits + (size_t(k.wpar) * cd.n_1 + q0) * 2 + c0;
+#pragma unroll
+                        for (int h = 0; h < LPT; ++h) {
+                            const uint32_t amh = (c0 + h) ? am1 : am0;
+                            wp[h] = (amh == FULL) ? bal[h] : ((bal[h] & amh) | (wp[h] & ~amh));
+                        }
+                    }
+                }
+            }
+        }
+    }
+    if (k.check && lane == 0) {
+        if (un0 & am0) atomicOr(&s_unsat[0], un0 & am0);
+        if (un1 & am1) atomicOr(&s_unsat[1], un1 & am1);
+    }
+    __syncthreads();
+    if (k.check && threadIdx.x < 2 && s_unsat[threadIdx.x]) atomicOr(g.unsat + threadIdx.x, s_unsat[threadIdx.x]);
+}
+
+// Generic class: any lane count, CNs with more than one degree-1 slot or total degree
+// 17..32 (rare in MET ensembles); one CN x one 32-lane chunk per warp item, run-time
+// degree, arrays in local memory.  Same arithmetic (N1).
+template <int RULE>
+__global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group g, CnCtl k, int begin, int count) {
+    using PT = PhiT<RULE>;
+    extern __shared__ __align__(16) char smem[];
+    __shared__ uint32_t s_unsat[4], s_act[4];
+    if (*reinterpret_cast<volatile int*>(g.done)) return;
+    load_phi_table<RULE>(smem, cd.phi);
+    if (threadIdx.x < g.C) { s_unsat[threadIdx.x] = 0u; s_act[threadIdx.x] = g.act[threadIdx.x]; }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const char* tabk = phi_tab_lane<RULE>(smem, lane);
+    const int wpb = blockDim.x >> 5;
+    const int lc = __ffs(g.C) - 1;
+    const long total = long(count) << lc;
+    for (long item = long(blockIdx.x) * wpb + (threadIdx.x >> 5); item < total; item += long(gridDim.x) * wpb) {
+        const int c = int(item & (g.C - 1));
+        const uint32_t amask = s_act[c];
+        if (!amask) continue;
+        const int j = begin + int(item >> lc);
+        const size_t off = size_t(c) * 32 + lane;
+        const int ab = __ldg(cd.cn_aptr + j), na = __ldg(cd.cn_aptr + j + 1) - ab;
+        const int db = __ldg(cd.cn_dptr + j), d = na + (__ldg(cd.cn_dptr + j + 1) - db);
+        const uint32_t sbit = (__ldg(g.synd_t + size_t(j) * g.C + c) >> lane) & 1u;
+        const int idx = (lane < na) ? __ldg(cd.a_vn + ab + lane) : 0;
+        float p[kMaxCnDeg], P[kMaxCnDeg], xs[kMaxCnDeg];
+        uint32_t negmask = 0, chk = sbit;
         for (int s = 0; s < d; ++s) {
             float x;
             if (s < na) {
                 const int v = __shfl_sync(FULL, idx, s);
-                const float Lv = __ldg(g.L + size_t(v) * B + off);
-                const float ro = k.first ? 0.0f : __ldcs(g.r + size_t(ab + s) * B + off);
-                x = __fsub_rn(Lv, ro);                                  // extrinsic, R10
-                chk ^= int(Lv < 0.0f);                                  // c_v^{l-1}, N4
+                const float Lv = __ldg(g.L + size_t(v) * g.B + off);
+                const float ro = k.first ? 0.0f : __ldcs(g.r + size_t(ab + s) * g.B + off);
+                x = __fsub_rn(Lv, ro);
+                chk ^= uint32_t(Lv < 0.0f);
             } else {
                 const int q = db + (s - na);
-                x = __ldcs(g.lam1 + size_t(q) * B + off);               // degree-1 VN sends its prior
-                lam1[s] = x;
-                if (k.check) chk ^= int((__ldg(g.d1bits + (size_t(k.rpar) * cd.n_1 + q) * C + c) >> lane) & 1u);
+                x = __ldcs(g.lam1 + size_t(q) * g.B + off);
+                if (k.check) chk ^= (__ldg(g.d1bits + (size_t(k.rpar) * cd.n_1 + q) * g.C + c) >> lane) & 1u;
             }
-            negmask |= uint32_t(x < 0.0f) << s;
-            p[s] = phi_dev<RULE>(tab, fabsf(x), cd.phi_top);
+            xs[s] = x;
+            negmask |= (__float_as_uint(__fadd_rn(x, 0.0f)) >> 31) << s;   // = [x < 0]
+            p[s] = phi_dev<RULE>(tabk, fabsf(x));
         }
         if (k.check) {
             const uint32_t mm = __ballot_sync(FULL, chk) & amask;
             if (mm && lane == 0) atomicOr(&s_unsat[c], mm);
         }
         float acc = 0.0f;
-#pragma unroll
         for (int s = 0; s < d; ++s) { P[s] = acc; acc = __fadd_rn(acc, p[s]); }
-        const uint32_t par = uint32_t(sbit) ^ (__popc(negmask) & 1u);
+        const uint32_t par = sbit ^ (__popc(negmask) & 1u);
         const bool act = (amask >> lane) & 1u;
         float Q = 0.0f;
-#pragma unroll
         for (int s = d - 1; s >= 0; --s) {
             const float S = __fadd_rn(P[s], Q);
-            const float mag = fminf(phi_dev<RULE>(tab, S, cd.phi_top), kRMax);
-            const float o = (par ^ ((negmask >> s) & 1u)) ? -mag : mag;
+            const float mag = fminf(phi_dev<RULE>(tabk, S), kRMax);
+            const float o = __uint_as_float(__float_as_uint(mag) | ((par ^ ((negmask >> s) & 1u)) << 31));
             if (s < na) {
-                if (act) __stcs(g.r + size_t(ab + s) * B + off, o);
+                if (act) __stcs(g.r + size_t(ab + s) * g.B + off, o);
             } else {
-                const int q = db + (s - na);
-                const uint32_t bal = __ballot_sync(FULL, __fadd_rn(lam1[s], o) < 0.0f);   // Step 5 for VN_b
+                const uint32_t bal = __ballot_sync(FULL, __fadd_rn(xs[s], o) < 0.0f);
                 if (lane == 0) {
-                    uint32_t* w = g.d1bits + (size_t(k.wpar) * cd.n_1 + q) * C + c;
+                    uint32_t* w = g.d1bits + (size_t(k.wpar) * cd.n_1 + db + (s - na)) * g.C + c;
                     *w = (amask == FULL) ? bal : ((bal & amask) | (*w & ~amask));
                 }
             }
-            Q = __fadd_rn(Q, p[s]);
-        }
-    }
-}
-
-template <int RULE, int D, int DHI>
-__device__ __forceinline__ void cn_dispatch(int d, const CodeDev& cd, const Group& g, const float* tab,
-                                            const CnCtl& k, int j, int c, int lane, uint32_t amask, int ab,
-                                            int na, int db, uint32_t* s_unsat) {
-    if constexpr (D <= DHI) {
-        if (d == D) {
-            cn_item<RULE, D, true>(cd, g, tab, k, j, c, lane, amask, ab, na, db, d, s_unsat);
-            return;
-        }
-        cn_dispatch<RULE, D + 1, DHI>(d, cd, g, tab, k, j, c, lane, amask, ab, na, db, s_unsat);
-    }
-}
-
-// One CN degree class (CNs with total degree in [DLO, DHI], listed in cls_cn).
-// DHI <= 16: unrolled per degree; DHI == 32: generic run-time-degree path.
-template <int RULE, int DLO, int DHI>
-__global__ void __launch_bounds__(256) k_cn_update(CodeDev cd, Group g, CnCtl k, const int32_t* __restrict__ cls_cn,
-                                                   int count) {
-    extern __shared__ __align__(16) float s_tab[];
-    __shared__ uint32_t s_unsat[4], s_act[4];
-    if (*reinterpret_cast<volatile int*>(g.done)) return;
-    constexpr int tabn4 = (RULE == METLDPC_RULE_EXACT) ? kPhiBins : kPhiBins / 2;   // float4 units
-    for (int i = threadIdx.x; i < tabn4; i += blockDim.x)
-        reinterpret_cast<float4*>(s_tab)[i] = __ldg(reinterpret_cast<const float4*>(cd.phi) + i);
-    if (threadIdx.x < g.C) { s_unsat[threadIdx.x] = 0u; s_act[threadIdx.x] = g.act[threadIdx.x]; }
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int wpb = blockDim.x >> 5;
-    const int lc = __ffs(g.C) - 1;  // C is a power of two
-    const long total = long(count) << lc;
-    for (long item = long(blockIdx.x) * wpb + (threadIdx.x >> 5); item < total; item += long(gridDim.x) * wpb) {
-        const int c = int(item & (g.C - 1));
-        const uint32_t amask = s_act[c];
-        if (!amask) continue;
-        const int j = __ldg(cls_cn + (item >> lc));
-        const int ab = __ldg(cd.cn_aptr + j), na = __ldg(cd.cn_aptr + j + 1) - ab;
-        const int db = __ldg(cd.cn_dptr + j), d = na + (__ldg(cd.cn_dptr + j + 1) - db);
-        if constexpr (DHI <= 16) {
-            cn_dispatch<RULE, DLO, DHI>(d, cd, g, s_tab, k, j, c, lane, amask, ab, na, db, s_unsat);
-        } else {
-            cn_item<RULE, DHI, false>(cd, g, s_tab, k, j, c, lane, amask, ab, na, db, d, s_unsat);
+            if (s > 0) Q = __fadd_rn(Q, p[s]);
         }
     }
     __syncthreads();
@@ -230,6 +410,111 @@ __global__ void __launch_bounds__(256) k_vn_update(CodeDev cd, Group g) {
         }
         if ((amask >> lane) & 1u) g.L[size_t(a) * B + off] = acc;
     }
+}
+
+// ------------------------------------------------------------------ 64-lane tiled VN update / check
+
+// Eq. (4)/(5), N3 for 64-lane groups: one warp per tile of 8 consecutive active VNs,
+// both 32-lane chunks per thread; the tile's column offsets are one coalesced load, each
+// column's CSC edge ids another (pre-scaled to row offsets), gathers batched 8 deep.
+__global__ void __launch_bounds__(256) k_vn_tile64(CodeDev cd, Group g) {
+    __shared__ uint32_t s_act[2];
+    if (*reinterpret_cast<volatile int*>(g.done)) return;
+    if (threadIdx.x < 2) s_act[threadIdx.x] = g.act[threadIdx.x];
+    __syncthreads();
+    const uint32_t am0 = s_act[0], am1 = s_act[1];
+    if (!(am0 | am1)) return;
+    const int lane = threadIdx.x & 31;
+    const bool act0 = (am0 >> lane) & 1u, act1 = (am1 >> lane) & 1u;
+    const int wpb = blockDim.x >> 5;
+    constexpr int TV = 8;     // VNs per warp tile (keeps every warp busy: n_a / 8 tiles)
+    const int ntiles = (cd.n_a + TV - 1) / TV;
+    const float* rl = g.r + lane;
+    for (int tile = blockIdx.x * wpb + (threadIdx.x >> 5); tile < ntiles; tile += gridDim.x * wpb) {
+        const int a0 = tile * TV;
+        const int nt = min(TV, cd.n_a - a0);
+        const int vb_l = lane < nt ? __ldg(cd.vn_aptr + a0 + lane) : 0;
+        const int ve_l = lane < nt ? __ldg(cd.vn_aptr + a0 + lane + 1) : 0;
+        for (int i = 0; i < nt; ++i) {
+            const int vb = __shfl_sync(FULL, vb_l, i), ve = __shfl_sync(FULL, ve_l, i);
+            const size_t row = size_t(a0 + i) * 64 + lane;
+            float acc0 = __ldg(g.lam_a + row), acc1 = __ldg(g.lam_a + row + 32);
+            for (int base = vb; base < ve; base += 32) {
+                const int cnt = min(32, ve - base);
+                const int eid = (lane < cnt) ? __ldg(cd.vn_aedge + base + lane) * 64 : 0;
+                int s = 0;
+                for (; s + 8 <= cnt; s += 8) {
+                    float v0[8], v1[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int e = __shfl_sync(FULL, eid, s + u);
+                        v0[u] = __ldcs(rl + e);
+                        v1[u] = __ldcs(rl + e + 32);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        acc0 = __fadd_rn(acc0, v0[u]);
+                        acc1 = __fadd_rn(acc1, v1[u]);
+                    }
+                }
+                for (; s < cnt; ++s) {
+                    const int e = __shfl_sync(FULL, eid, s);
+                    acc0 = __fadd_rn(acc0, __ldcs(rl + e));
+                    acc1 = __fadd_rn(acc1, __ldcs(rl + e + 32));
+                }
+            }
+            if (act0) g.L[row] = acc0;
+            if (act1) g.L[row + 32] = acc1;
+        }
+    }
+}
+
+// Syndrome test of iteration l = N (N4) for 64-lane groups: warp per tile of 32 CNs.
+__global__ void __launch_bounds__(256) k_check64(CodeDev cd, Group g, int par) {
+    __shared__ uint32_t s_unsat[2], s_act[2];
+    if (threadIdx.x < 2) { s_unsat[threadIdx.x] = 0u; s_act[threadIdx.x] = g.act[threadIdx.x]; }
+    __syncthreads();
+    const uint32_t am0 = s_act[0], am1 = s_act[1];
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    const int ntiles = (cd.m + 31) >> 5;
+    const float* Ll = g.L + lane;
+    uint32_t un0 = 0, un1 = 0;
+    if (am0 | am1) {
+        for (int tile = blockIdx.x * wpb + (threadIdx.x >> 5); tile < ntiles; tile += gridDim.x * wpb) {
+            const int j0 = tile * 32;
+            const int nt = min(32, cd.m - j0);
+            const bool on = lane < nt;
+            const int a_l = on ? __ldg(cd.cn_aptr + j0 + lane) : 0, ae_l = on ? __ldg(cd.cn_aptr + j0 + lane + 1) : 0;
+            const int d_l = on ? __ldg(cd.cn_dptr + j0 + lane) : 0, de_l = on ? __ldg(cd.cn_dptr + j0 + lane + 1) : 0;
+            const uint2 sw_l = on ? __ldg(reinterpret_cast<const uint2*>(g.synd_t) + (j0 + lane)) : make_uint2(0, 0);
+            for (int i = 0; i < nt; ++i) {
+                const int ab = __shfl_sync(FULL, a_l, i), na = __shfl_sync(FULL, ae_l, i) - ab;
+                const int db = __shfl_sync(FULL, d_l, i), nd = __shfl_sync(FULL, de_l, i) - db;
+                uint32_t c0 = (__shfl_sync(FULL, sw_l.x, i) >> lane) & 1u;
+                uint32_t c1 = (__shfl_sync(FULL, sw_l.y, i) >> lane) & 1u;
+                const int idx = (lane < na) ? __ldg(cd.a_vn + ab + lane) * 64 : 0;
+                for (int s = 0; s < na; ++s) {
+                    const int o = __shfl_sync(FULL, idx, s);
+                    c0 ^= uint32_t(__ldg(Ll + o) < 0.0f);
+                    c1 ^= uint32_t(__ldg(Ll + o + 32) < 0.0f);
+                }
+                for (int q = db; q < db + nd; ++q) {
+                    const uint2 w = __ldg(reinterpret_cast<const uint2*>(g.d1bits) + (size_t(par) * cd.n_1 + q));
+                    c0 ^= (w.x >> lane) & 1u;
+                    c1 ^= (w.y >> lane) & 1u;
+                }
+                un0 |= __ballot_sync(FULL, c0);
+                un1 |= __ballot_sync(FULL, c1);
+            }
+        }
+    }
+    if (lane == 0) {
+        if (un0 & am0) atomicOr(&s_unsat[0], un0 & am0);
+        if (un1 & am1) atomicOr(&s_unsat[1], un1 & am1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 && s_unsat[threadIdx.x]) atomicOr(g.unsat + threadIdx.x, s_unsat[threadIdx.x]);
 }
 
 // ------------------------------------------------------------------ latch (a4 bookkeeping)
@@ -306,7 +591,7 @@ __global__ void __launch_bounds__(256) k_pack_syndrome(CodeDev cd, Group g, cons
         if (lane == b) mine = bal;
     }
     const int j = wd * 32 + lane;
-    if (j < cd.m) g.synd_t[size_t(j) * g.C + c] = mine;
+    if (j < cd.m) g.synd_t[size_t(__ldg(cd.cn_new + j)) * g.C + c] = mine;
 }
 
 __global__ void k_init_ctl(Group g, int nb) {
@@ -419,46 +704,54 @@ void launch_counters(int batch, const int32_t* iters, const uint8_t* conv, int64
 
 // ------------------------------------------------------------------ launchers
 
-template <int RULE, int W>
-static void* cn_fn() { return reinterpret_cast<void*>(&k_cn_update<RULE, kCnWinLo[W], kCnWinHi[W]>); }
+template <int RULE, int NA, int ND>
+static void* cn_tile_fn() { return reinterpret_cast<void*>(&k_cn_tile<RULE, NA, ND>); }
 
-template <int RULE>
-static void* cn_kernel_rule(int win) {
-    switch (win) {
-        case 0: return cn_fn<RULE, 0>();
-        case 1: return cn_fn<RULE, 1>();
-        case 2: return cn_fn<RULE, 2>();
-        case 3: return cn_fn<RULE, 3>();
-        default: return cn_fn<RULE, 4>();
+template <int RULE, int D = 0>
+static void* cn_tile_kernel(int d, int nd) {
+    if constexpr (D <= kMaxUnrolledCnDeg) {
+        if (d == D) {
+            if constexpr (D == 0) return cn_tile_fn<RULE, 0, 0>();
+            else return nd ? cn_tile_fn<RULE, D - 1, 1>() : cn_tile_fn<RULE, D, 0>();
+        }
+        return cn_tile_kernel<RULE, D + 1>(d, nd);
+    } else {
+        return nullptr;
     }
 }
 
-static void* cn_kernel(int rule, int win) {
-    return rule == METLDPC_RULE_EXACT ? cn_kernel_rule<METLDPC_RULE_EXACT>(win)
-                                      : cn_kernel_rule<METLDPC_RULE_PHI_LUT>(win);
+static void* cn_kernel(int rule, int D, int nd) {
+    if (D < 0)
+        return rule == METLDPC_RULE_EXACT ? reinterpret_cast<void*>(&k_cn_generic<METLDPC_RULE_EXACT>)
+                                          : reinterpret_cast<void*>(&k_cn_generic<METLDPC_RULE_PHI_LUT>);
+    return rule == METLDPC_RULE_EXACT ? cn_tile_kernel<METLDPC_RULE_EXACT>(D, nd)
+                                      : cn_tile_kernel<METLDPC_RULE_PHI_LUT>(D, nd);
 }
 
-static size_t cn_smem(int rule) {
-    return size_t(kPhiBins) * (rule == METLDPC_RULE_EXACT ? 4 : 2) * sizeof(float);
+int cn_tile_max(int D, int nd) { return (D - nd) <= 4 ? 32 : 8; }
+int cn_units_per_tile(int D, int nd) { return (D - nd) <= 4 ? 1 : 2; }
+
+size_t cn_smem(int rule, int D, int nd) {
+    const size_t tab = size_t(rule == METLDPC_RULE_EXACT ? PhiT<METLDPC_RULE_EXACT>::TAB_BYTES
+                                                         : PhiT<METLDPC_RULE_PHI_LUT>::TAB_BYTES);
+    if (D < 0) return tab;
+    const int na = std::max(1, D - nd);
+    return tab + size_t(kCnThreads / 32) * cn_tile_max(D, nd) * na * sizeof(int);
 }
 
-int cn_window(int dlo) {
-    for (int w = 0; w < kNumCnWindows; ++w)
-        if (kCnWinLo[w] == dlo) return w;
-    return kNumCnWindows - 1;
-}
-
-int cn_blocks_per_sm(int rule, int win) {
+int cn_blocks_per_sm(int rule, int D, int nd) {
     int nb = 0;
-    void* f = cn_kernel(rule, win);
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cn_smem(rule)));
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, 256, cn_smem(rule)) != cudaSuccess) nb = 1;
+    void* f = cn_kernel(rule, D, nd);
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cn_smem(rule, D, nd)));
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kCnThreads, cn_smem(rule, D, nd)) != cudaSuccess) nb = 1;
     return nb > 0 ? nb : 1;
 }
 
 int vn_blocks_per_sm() {
-    int nb = 0;
+    int nb = 0, nb2 = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_vn_update, 256, 0) != cudaSuccess) nb = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, k_vn_tile64, 256, 0) != cudaSuccess) nb2 = 1;
+    nb = std::min(nb, nb2);
     return nb > 0 ? nb : 1;
 }
 
@@ -474,20 +767,27 @@ void launch_pack_syndrome(const CodeDev& cd, const Group& g, const uint32_t* syn
 
 void launch_init_ctl(const Group& g, int nb, cudaStream_t s) { k_init_ctl<<<1, 128, 0, s>>>(g, nb); }
 
-void launch_cn(const CodeDev& cd, const Group& g, int rule, int win, const int32_t* cls_cn, int count, int grid,
+void launch_cn(const CodeDev& cd, const Group& g, int rule, int D, int nd, int begin, int count, int ts, int grid,
                int l, bool check, cudaStream_t s) {
     CnCtl k{check ? 1 : 0, l == 1 ? 1 : 0, (l - 1) & 1, l & 1};
-    void* f = cn_kernel(rule, win);
-    void* args[] = {const_cast<CodeDev*>(&cd), const_cast<Group*>(&g), &k, const_cast<int32_t**>(&cls_cn), &count};
-    cudaLaunchKernel(f, dim3(grid), dim3(256), args, cn_smem(rule), s);
+    void* f = cn_kernel(rule, D, nd);
+    if (D < 0) {
+        void* args[] = {const_cast<CodeDev*>(&cd), const_cast<Group*>(&g), &k, &begin, &count};
+        cudaLaunchKernel(f, dim3(grid), dim3(kCnThreads), args, cn_smem(rule, D, nd), s);
+    } else {
+        void* args[] = {const_cast<CodeDev*>(&cd), const_cast<Group*>(&g), &k, &begin, &count, &ts};
+        cudaLaunchKernel(f, dim3(grid), dim3(kCnThreads), args, cn_smem(rule, D, nd), s);
+    }
 }
 
 void launch_vn(const CodeDev& cd, const Group& g, int grid, cudaStream_t s) {
-    k_vn_update<<<grid, 256, 0, s>>>(cd, g);
+    if (g.B == 64) k_vn_tile64<<<grid, 256, 0, s>>>(cd, g);
+    else k_vn_update<<<grid, 256, 0, s>>>(cd, g);
 }
 
 void launch_check(const CodeDev& cd, const Group& g, int grid, int l, cudaStream_t s) {
-    k_check<<<grid, 256, 0, s>>>(cd, g, l & 1);
+    if (g.B == 64) k_check64<<<grid, 256, 0, s>>>(cd, g, l & 1);
+    else k_check<<<grid, 256, 0, s>>>(cd, g, l & 1);
 }
 
 void launch_latch(const Group& g, int l, bool final_, cudaStream_t s) { k_latch<<<1, 32, 0, s>>>(g, l, final_ ? 1 : 0); }
@@ -509,3 +809,7 @@ void launch_md_llr(int64_t total, int n, int d, float c, const float* v, const f
 }
 
 }  // namespace metldpc
+
+namespace metldpc {
+const int kCnThreadsHost = kCnThreads;
+}

@@ -36,19 +36,25 @@ struct CodeDev {
     const int32_t* vn_aptr;
     const int32_t* vn_aedge;
     const int32_t* vmap;
+    const int32_t* cn_new;  // original CN id -> relabelled id
     const float* phi;      // table of the selected rule
     float phi_top;
 };
 
 // returns the number of CTAs per SM the CN kernel reaches (for persistent grids)
-int cn_window(int dlo);                      // index of the degree window starting at dlo
-int cn_blocks_per_sm(int rule, int win);
+// CN class kernels: total degree D in 0..16 with nd <= 1 degree-1 slots (tiled, unrolled)
+// or D = -1 (generic: more degree-1 slots or degree 17..32)
+int cn_blocks_per_sm(int rule, int D, int nd);
+int cn_tile_max(int D, int nd);          // CNs per warp tile the kernel stages
+int cn_units_per_tile(int D, int nd);    // warp units per tile (1: both chunks, 2: one each)
+extern const int kCnThreadsHost;
+size_t cn_smem(int rule, int D);
 int vn_blocks_per_sm();
 
 void launch_scatter(const CodeDev& cd, const Group& g, const float* llr, int nb, cudaStream_t s);
 void launch_pack_syndrome(const CodeDev& cd, const Group& g, const uint32_t* synd, int nb, cudaStream_t s);
 void launch_init_ctl(const Group& g, int nb, cudaStream_t s);
-void launch_cn(const CodeDev& cd, const Group& g, int rule, int win, const int32_t* cls_cn, int count, int grid,
+void launch_cn(const CodeDev& cd, const Group& g, int rule, int D, int nd, int begin, int count, int ts, int grid,
                int l, bool check, cudaStream_t s);
 void launch_vn(const CodeDev& cd, const Group& g, int grid, cudaStream_t s);
 void launch_check(const CodeDev& cd, const Group& g, int grid, int l, cudaStream_t s);

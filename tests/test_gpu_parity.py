@@ -184,11 +184,16 @@ def test_generic_degree_paths_and_alist(tmp_path):
     """Random codes exercising every CN-degree window (0-4, 5-8, 9-12, 13-16, 17-32),
     loaded through alist, against the oracle."""
     rng = np.random.default_rng(21)
-    for t, (n, m, deg) in enumerate([(60, 20, (2, 3)), (80, 12, (2, 4)), (120, 10, (2, 4)), (200, 8, (2, 3))]):
-        code = random_code(n, m, rng, frac_deg1=0.3, act_deg=deg)
+    windows = set()
+    for t, (n, m, deg) in enumerate([(60, 20, (2, 3)), (80, 12, (2, 4)), (120, 12, (2, 3)), (90, 16, (2, 3))]):
+        for _ in range(100):
+            code = random_code(n, m, rng, frac_deg1=0.3, act_deg=deg)
+            if code.cn_degree.max() <= 32:
+                break
         p = tmp_path / f"c{t}.alist"
         write_alist(code, p)
         h = B.Code(alist=str(p))
+        windows.update(int(np.searchsorted([4, 8, 12, 16, 32], d)) for d in code.cn_degree)
         assert h.info.edges == code.num_edges and h.info.max_cn_deg == code.cn_degree.max()
         u = rng.integers(0, 2, n).astype(np.uint8)
         s = (code.dense().astype(int) @ u) % 2
@@ -200,6 +205,7 @@ def test_generic_degree_paths_and_alist(tmp_path):
             for i in range(8):
                 o = bp.decode(code, llr[i], synd[i], 30, rule=rule, prec=32)
                 _assert_frame_equal(code, o, bits[i], iters[i], conv[i], f"code {t} frame {i}")
+    assert windows == {0, 1, 2, 3, 4}, windows
 
 
 def test_empty_check_row():

@@ -1,0 +1,71 @@
+#!/usr/bin/env python
+"""Summarise ncu launch lists and full captures into the tables committed under profiles/.
+
+    python tools/ncu_summary.py launches <launches.csv>      # per-kernel time and share of the step
+    python tools/ncu_summary.py metrics <capture.ncu-rep>    # key roofline metrics per captured launch
+"""
+import csv
+import io
+import re
+import subprocess
+import sys
+from collections import OrderedDict
+
+
+def _short(name: str) -> str:
+    name = re.sub(r"\(metldpc::CodeDev.*$|\(CodeDev.*$", "", name)
+    name = name.replace("metldpc::", "").replace("void ", "")
+    return name.strip()
+
+
+def launches(path: str) -> str:
+    rows = list(csv.reader(open(path)))
+    start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    hdr = rows[start]
+    ik, iv, iu = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    agg = OrderedDict()
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
+    for r in rows[start + 1:]:
+        if len(r) < len(hdr):
+            continue
+        v = float(r[iv].replace(",", "")) * scale.get(r[iu], 1.0)
+        k = _short(r[ik])
+        n, t = agg.get(k, (0, 0.0))
+        agg[k] = (n + 1, t + v)
+    tot = sum(t for _, t in agg.values())
+    out = io.StringIO()
+    out.write(f"{'launches':>8} {'total us':>12} {'mean us':>10} {'share':>7}  kernel\n")
+    for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        out.write(f"{n:8d} {t:12.1f} {t / n:10.1f} {100 * t / tot:6.1f}%  {k}\n")
+    out.write(f"{'':8s} {tot:12.1f} us total (ncu-serialised, cold-cache per launch)\n")
+    return out.getvalue()
+
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "smsp__inst_executed.sum", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "l1tex__throughput.avg.pct_of_peak_sustained_active", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+        "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
+        "launch__registers_per_thread", "launch__grid_size", "launch__block_size", "sm__cycles_elapsed.avg.per_second"]
+
+
+def metrics(path: str) -> str:
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    out = io.StringIO()
+    for r in rows[2:]:
+        out.write(_short(r[hdr.index("Kernel Name")]) + "\n")
+        for k in KEYS:
+            if k in hdr:
+                out.write(f"    {k:62s} {r[hdr.index(k)]:>16s} {units[hdr.index(k)]}\n")
+        rb = float(r[hdr.index("dram__bytes_read.sum")]) * (1e9 if units[hdr.index("dram__bytes_read.sum")] == "Gbyte" else 1e6 if units[hdr.index("dram__bytes_read.sum")] == "Mbyte" else 1)
+        wb = float(r[hdr.index("dram__bytes_write.sum")]) * (1e9 if units[hdr.index("dram__bytes_write.sum")] == "Gbyte" else 1e6 if units[hdr.index("dram__bytes_write.sum")] == "Mbyte" else 1)
+        out.write(f"    {'dram bytes (read + write)':62s} {rb + wb:16.0f} byte\n")
+    return out.getvalue()
+
+
+if __name__ == "__main__":
+    mode, path = sys.argv[1], sys.argv[2]
+    sys.stdout.write(launches(path) if mode == "launches" else metrics(path))
