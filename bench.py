@@ -215,6 +215,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_1711_01783_b200 import binding as B
+    from paper_1711_01783_b200 import dist as D
     from paper_1711_01783_b200 import metrics
     from paper_1711_01783_b200.build import build
     from synth.codes import make_met_code
@@ -231,11 +232,11 @@ def main():
     code = make_met_code(a.family, a.n)
     st = code.stats()
     F = a.frames
-    # frames of this rank: global ids f = rank + world * k; D distinct ones tiled to F
-    D = min(a.distinct, F)
-    ids = [rank + world * k for k in range(D)]
+    # frames of this rank: global ids f with f mod world == rank; ND distinct ones tiled to F
+    ND = min(a.distinct, F)
+    ids = D.shard_frames(range(ND * world), rank, world)
     v_np, xn_np, sy_np = gen_frames(a, ids)
-    rep = (F + D - 1) // D
+    rep = (F + ND - 1) // ND
     v = torch.from_numpy(np.tile(v_np, (rep, 1))[:F]).to(dev)
     xn = torch.from_numpy(np.tile(xn_np, (rep, 1))[:F]).to(dev)
     sy = torch.from_numpy(np.tile(sy_np, (rep, 1))[:F].view(np.int32)).to(dev)
@@ -254,8 +255,7 @@ def main():
         dec.llr_from_md(v, xn, a.snr, out=llr)
         dec.decode(llr, sy, out=(bits, iters, conv))
         dec.counters(iters, conv, cnt)
-        if world > 1:
-            dist.all_reduce(cnt)
+        D.reduce_counters(cnt)          # NCCL all-reduce when world > 1 (the only exchange)
 
     for _ in range(max(a.warmup, 0)):
         step()
@@ -282,11 +282,7 @@ def main():
     clocks = sampler.stop() if sampler else None
     dec.set_profiling(False)
     prof = dec.profile()
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = D.max_over_ranks(e0.elapsed_time(e1), device=dev)
     counters = cnt.cpu().numpy()   # all-reduced in-step when world > 1 (sum over ranks of K steps)
     if world == 1:
         pass
@@ -332,11 +328,9 @@ def main():
         t0 = time.perf_counter()
         for _ in range(k_e2e):
             dec.decode_md_host(v_h, xn_h, sy_h, a.snr, out=out_h)
-        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        dt = D.max_over_ranks(time.perf_counter() - t0, device=dev)
         W = (st["m"] + 31) // 32
-        e2e = {"value": F * world * k_e2e * a.n / float(dt.item()) / 1e6, "unit": "Mb/s",
+        e2e = {"value": F * world * k_e2e * a.n / dt / 1e6, "unit": "Mb/s",
                "h2d_bytes_per_step": F * world * (a.n * 4 + (a.n // 8) * 4 + W * 4),
                "d2h_bytes_per_step": F * world * (nw * 4 + 4 + 1),
                "api": "metldpc_decode_md_host (pinned host buffers; H2D, LLR, decode, D2H per 64-lane group, "
@@ -356,7 +350,7 @@ def main():
             "config": {"workload": workload_name(a), "code": f"{a.family} stand-in (Table-1 counts), n={a.n}, "
                        f"m={st['m']}, E={st['edges']}, E_it={st['iter_edges']}", "snr": a.snr,
                        "beta": metrics.beta(R, a.snr), "max_iter": a.iters, "early_term": not a.no_et,
-                       "rule": a.rule.upper(), "frames_per_gpu": F, "distinct_frames_per_gpu": D,
+                       "rule": a.rule.upper(), "frames_per_gpu": F, "distinct_frames_per_gpu": ND,
                        "lanes_per_group": a.lanes, "global_batch": F * world,
                        "l2": "inputs larger than L2 (v 1 GB, edge messages 740 MB per 64-lane group)",
                        "parallelism": f"dp{world} (frames sharded f mod G; NCCL all-reduce of FER counters)"},
