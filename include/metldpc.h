@@ -60,6 +60,9 @@ typedef struct {
                                   0 = fixed N, the paper's Figure-1 flow               */
     int32_t lanes_per_group;   /* codewords interleaved per group: 32, 64 or 128; default 64
                                   (coalesced when a multiple of 32)               */
+    int32_t groups_in_flight;  /* lane groups decoded concurrently on their own streams, 1..8;
+                                  default 4 (each has its own ~1 GB workspace at C3; their
+                                  kernels fill each other's ramps, tails and launch gaps)   */
 } metldpc_config_t;
 
 typedef struct {
@@ -120,11 +123,12 @@ void metldpc_code_destroy(metldpc_code code);
 
 void metldpc_config_default(metldpc_config_t* cfg);
 
-/* Workspace for batches of up to max_batch frames.  Frames are decoded one lane group
- * (lanes_per_group frames) after another through ONE group workspace (~ E_it x lanes x 4 B
- * of edge messages plus node arrays: ~1.05 GB for the rate-0.1 n = 10^6 code at 64 lanes),
- * so device memory does not grow with max_batch; the host-buffer paths add two group
- * staging slots on first use.  cfg may be NULL (defaults). */
+/* Workspace for batches of up to max_batch frames.  Frames are decoded in lane groups
+ * (lanes_per_group frames), groups_in_flight groups at a time, each through its own group
+ * workspace (~ E_it x lanes x 4 B of edge messages plus node arrays: ~1.05 GB for the
+ * rate-0.1 n = 10^6 code at 64 lanes), so device memory does not grow with max_batch; the
+ * host-buffer paths add 2 x groups_in_flight staging slots on first use.  cfg may be NULL
+ * (defaults). */
 metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch,
                                       const metldpc_config_t* cfg, metldpc_decoder* out);
 void metldpc_decoder_destroy(metldpc_decoder dec);

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -41,19 +42,31 @@ struct metldpc_decoder_s {
     struct ClassLaunch { int D, nd; int32_t begin, count; int ts, grid; };
     std::vector<ClassLaunch> cn_classes;
     int vn_grid = 0, chk_grid = 0;
-    // one group workspace
-    float *r = nullptr, *L = nullptr, *lam_a = nullptr, *lam1 = nullptr;
-    uint32_t *d1bits = nullptr, *synd_t = nullptr, *ctl = nullptr;  // ctl: act[4] unsat[4] invalid[4]
-    int32_t* iters = nullptr;
-    uint8_t* conv = nullptr;
-    int32_t* done = nullptr;
-    // host-path staging (2 slots of one group each)
-    float* st_llr[2] = {nullptr, nullptr};
-    uint32_t* st_synd[2] = {nullptr, nullptr};
-    uint32_t* st_bits[2] = {nullptr, nullptr};
-    int32_t* st_iters[2] = {nullptr, nullptr};
-    uint8_t* st_conv[2] = {nullptr, nullptr};
-    float* st_xnorm[2] = {nullptr, nullptr};
+    // K lane-group workspaces decoded concurrently on K streams (their CN and VN kernels
+    // interleave on the GPU: the issue-bound CN pass of one group overlaps the HBM-bound VN
+    // pass of another).
+    struct Workspace {
+        float *r = nullptr, *L = nullptr, *lam_a = nullptr, *lam1 = nullptr;
+        uint32_t *d1bits = nullptr, *synd_t = nullptr, *ctl = nullptr;  // ctl: act[4] unsat[4] invalid[4]
+        int32_t* iters = nullptr;
+        uint8_t* conv = nullptr;
+        int32_t* done = nullptr;
+    };
+    int K = 1;
+    std::vector<Workspace> ws;
+    std::vector<cudaStream_t> gs;                   // one stream per workspace (K > 1)
+    std::vector<cudaEvent_t> fork_ev, join_ev;
+    int last_ws = 0;                                // workspace of the last group decoded
+    // host-path staging: 2 rounds x K groups
+    struct Staging {
+        float* llr = nullptr;
+        uint32_t* synd = nullptr;
+        uint32_t* bits = nullptr;
+        int32_t* iters = nullptr;
+        uint8_t* conv = nullptr;
+        float* xnorm = nullptr;
+    };
+    std::vector<Staging> st;
     cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
     // accounting
     int profiling = 0;
@@ -103,22 +116,23 @@ CodeDev code_dev(const metldpc_code c, int rule) {
     return cd;
 }
 
-Group group_of(metldpc_decoder d) {
+Group group_of(metldpc_decoder d, int k) {
+    const auto& w = d->ws[size_t(k)];
     Group g;
     g.B = d->B;
     g.C = d->C;
-    g.r = d->r;
-    g.L = d->L;
-    g.lam_a = d->lam_a;
-    g.lam1 = d->lam1;
-    g.d1bits = d->d1bits;
-    g.synd_t = d->synd_t;
-    g.act = d->ctl;
-    g.unsat = d->ctl + 4;
-    g.invalid = d->ctl + 8;
-    g.iters = d->iters;
-    g.conv = d->conv;
-    g.done = d->done;
+    g.r = w.r;
+    g.L = w.L;
+    g.lam_a = w.lam_a;
+    g.lam1 = w.lam1;
+    g.d1bits = w.d1bits;
+    g.synd_t = w.synd_t;
+    g.act = w.ctl;
+    g.unsat = w.ctl + 4;
+    g.invalid = w.ctl + 8;
+    g.iters = w.iters;
+    g.conv = w.conv;
+    g.done = w.done;
     return g;
 }
 
@@ -143,6 +157,16 @@ metldpc_status check_device(int32_t device, int* num_sms) {
     if (p.major != 10) return fail(METLDPC_EUNSUPPORTED, std::string("built for sm_100a; device is ") + p.name);
     *num_sms = p.multiProcessorCount;
     return METLDPC_OK;
+}
+
+// Resident-CTA share of each persistent kernel when K groups are in flight.  Measured
+// (round 1, C3): sizing every kernel for the whole GPU (split 1) beats splitting the SMs
+// between the groups -- the gain of K > 1 is filling each kernel's ramp/tail and the
+// launch gaps with another group's work.  METLDPC_GRID_SPLIT overrides (experiments).
+int grid_split(int /*K*/) {
+    const char* e = std::getenv("METLDPC_GRID_SPLIT");
+    if (e && *e) return std::max(1, std::atoi(e));
+    return 1;
 }
 
 // Records a kernel-timing event pair when profiling (CUDA events on the launch stream).
@@ -177,42 +201,96 @@ void ev_collect(metldpc_decoder d) {
     d->ev_used = 0;
 }
 
-// One lane group of nb <= B frames; pointers already offset to the group's first frame.
-metldpc_status decode_group(metldpc_decoder d, const float* llr, const uint32_t* synd, int nb, int N,
-                            uint32_t* bits_out, int32_t* iters_out, uint8_t* conv_out, cudaStream_t s) {
-    const metldpc_code c = d->code;
-    const CodeDev cd = code_dev(c, d->cfg.rule);
-    const Group g = group_of(d);
-    const bool et = d->cfg.early_term != 0;
-    CUDA_TRY(cudaMemsetAsync(d->ctl + 8, 0, 4 * sizeof(uint32_t), s));
-    launch_scatter(cd, g, llr, nb, s);
-    launch_pack_syndrome(cd, g, synd, nb, s);
-    launch_init_ctl(g, nb, s);
+// A lane group in three phases so K groups can be interleaved on K streams.
+struct GroupJob {
+    int k;                       // workspace
+    const float* llr;            // frame-major inputs, offset to the group's first frame
+    const uint32_t* synd;
+    int nb;                      // frames in the group (<= B)
+    uint32_t* bits_out;
+    int32_t* iters_out;
+    uint8_t* conv_out;
+    cudaStream_t s;
+    cudaEvent_t ready = nullptr;   // optional: inputs staged (host path); waited on by the group's stream
+    cudaEvent_t done = nullptr;    // optional: recorded on the group's stream after finalize
+};
+
+metldpc_status group_begin(metldpc_decoder d, const GroupJob& j) {
+    const CodeDev cd = code_dev(d->code, d->cfg.rule);
+    const Group g = group_of(d, j.k);
+    CUDA_TRY(cudaMemsetAsync(d->ws[size_t(j.k)].ctl + 8, 0, 4 * sizeof(uint32_t), j.s));
+    launch_scatter(cd, g, j.llr, j.nb, j.s);
+    launch_pack_syndrome(cd, g, j.synd, j.nb, j.s);
+    launch_init_ctl(g, j.nb, j.s);
     d->prof.launches += 3;
-    for (int l = 1; l <= N; ++l) {
-        size_t e = ev_begin(d, 0, s);
-        for (const auto& k : d->cn_classes) {
-            launch_cn(cd, g, d->cfg.rule, k.D, k.nd, k.begin, k.count, k.ts, k.grid, l, et && l >= 2, s);
-            d->prof.launches++;
-        }
-        ev_end(d, e, s);
-        d->prof.cn_launches++;
-        d->prof.cn_lane_iters += nb;
-        if (et && l >= 2) {
-            launch_latch(g, l - 1, false, s);
-            d->prof.launches++;
-        }
-        e = ev_begin(d, 1, s);
-        launch_vn(cd, g, d->vn_grid, s);
-        ev_end(d, e, s);
-        d->prof.vn_launches++;
+    return METLDPC_OK;
+}
+
+// Iteration l: CN update (all degree classes; tests iteration l-1 when ET is on), latch,
+// VN update.
+void group_iter(metldpc_decoder d, const GroupJob& j, int l) {
+    const CodeDev cd = code_dev(d->code, d->cfg.rule);
+    const Group g = group_of(d, j.k);
+    const bool et = d->cfg.early_term != 0;
+    size_t e = ev_begin(d, 0, j.s);
+    for (const auto& c : d->cn_classes) {
+        launch_cn(cd, g, d->cfg.rule, c.D, c.nd, c.begin, c.count, c.ts, c.grid, l, et && l >= 2, j.s);
         d->prof.launches++;
     }
-    launch_check(cd, g, d->chk_grid, N, s);
-    launch_latch(g, N, true, s);
-    launch_finalize(cd, g, nb, bits_out, iters_out, conv_out, s);
+    ev_end(d, e, j.s);
+    d->prof.cn_launches++;
+    d->prof.cn_lane_iters += j.nb;
+    if (et && l >= 2) {
+        launch_latch(g, l - 1, false, j.s);
+        d->prof.launches++;
+    }
+    e = ev_begin(d, 1, j.s);
+    launch_vn(cd, g, d->vn_grid, j.s);
+    ev_end(d, e, j.s);
+    d->prof.vn_launches++;
+    d->prof.launches++;
+}
+
+metldpc_status group_end(metldpc_decoder d, const GroupJob& j, int N) {
+    const CodeDev cd = code_dev(d->code, d->cfg.rule);
+    const Group g = group_of(d, j.k);
+    launch_check(cd, g, d->chk_grid, N, j.s);
+    launch_latch(g, N, true, j.s);
+    launch_finalize(cd, g, j.nb, j.bits_out, j.iters_out, j.conv_out, j.s);
     d->prof.launches += 3;
+    d->last_ws = j.k;
     CUDA_TRY(cudaGetLastError());
+    return METLDPC_OK;
+}
+
+// Decodes up to K groups concurrently: forked from stream `s` onto the workspace streams,
+// iterations interleaved group by group, joined back into `s`.
+metldpc_status decode_round(metldpc_decoder d, std::vector<GroupJob>& jobs, int N, cudaStream_t s) {
+    metldpc_status st;
+    if (jobs.size() == 1) {
+        jobs[0].s = s;
+        if (jobs[0].ready) CUDA_TRY(cudaStreamWaitEvent(s, jobs[0].ready, 0));
+        if ((st = group_begin(d, jobs[0]))) return st;
+        for (int l = 1; l <= N; ++l) group_iter(d, jobs[0], l);
+        if ((st = group_end(d, jobs[0], N))) return st;
+        if (jobs[0].done) CUDA_TRY(cudaEventRecord(jobs[0].done, s));
+        return METLDPC_OK;
+    }
+    CUDA_TRY(cudaEventRecord(d->fork_ev[0], s));
+    for (auto& j : jobs) {
+        j.s = d->gs[size_t(j.k)];
+        CUDA_TRY(cudaStreamWaitEvent(j.s, d->fork_ev[0], 0));
+        if (j.ready) CUDA_TRY(cudaStreamWaitEvent(j.s, j.ready, 0));
+        if ((st = group_begin(d, j))) return st;
+    }
+    for (int l = 1; l <= N; ++l)
+        for (auto& j : jobs) group_iter(d, j, l);
+    for (auto& j : jobs) {
+        if ((st = group_end(d, j, N))) return st;
+        if (j.done) CUDA_TRY(cudaEventRecord(j.done, j.s));
+        CUDA_TRY(cudaEventRecord(d->join_ev[size_t(j.k)], j.s));
+        CUDA_TRY(cudaStreamWaitEvent(s, d->join_ev[size_t(j.k)], 0));
+    }
     return METLDPC_OK;
 }
 
@@ -291,6 +369,7 @@ void metldpc_config_default(metldpc_config_t* cfg) {
     cfg->max_iter = 100;
     cfg->early_term = 1;
     cfg->lanes_per_group = 64;
+    cfg->groups_in_flight = 4;
 }
 
 metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, const metldpc_config_t* cfg_in,
@@ -304,6 +383,7 @@ metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, cons
     if (cfg.max_iter < 1) return fail(METLDPC_EINVAL, "max_iter must be >= 1");
     if (cfg.lanes_per_group != 32 && cfg.lanes_per_group != 64 && cfg.lanes_per_group != 128)
         return fail(METLDPC_EINVAL, "lanes_per_group must be 32, 64 or 128");
+    if (cfg.groups_in_flight < 1 || cfg.groups_in_flight > 8) return fail(METLDPC_EINVAL, "groups_in_flight must be 1..8");
     if (max_batch < 1) return fail(METLDPC_EINVAL, "max_batch must be >= 1");
     if ((code->host.E_it + 1) * int64_t(cfg.lanes_per_group) >= (int64_t(1) << 31) ||
         (int64_t(code->host.n_a) + 1) * cfg.lanes_per_group >= (int64_t(1) << 31))
@@ -319,16 +399,29 @@ metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, cons
     const HostLayout& L = code->host;
     const size_t B = size_t(d->B), C = size_t(d->C);
     metldpc_status s;
-    if ((s = dalloc(&d->r, size_t(L.E_it) * B)) || (s = dalloc(&d->L, size_t(L.n_a) * B)) ||
-        (s = dalloc(&d->lam_a, size_t(L.n_a) * B)) || (s = dalloc(&d->lam1, size_t(L.n_1) * B)) ||
-        (s = dalloc(&d->d1bits, 2 * size_t(L.n_1) * C)) || (s = dalloc(&d->synd_t, size_t(L.m) * C)) ||
-        (s = dalloc(&d->ctl, 16)) || (s = dalloc(&d->iters, B)) || (s = dalloc(&d->conv, B)) ||
-        (s = dalloc(&d->done, 1))) {
-        metldpc_decoder_destroy(d);
-        return s;
+    // groups in flight: never more than the batch needs
+    d->K = std::max(1, std::min(cfg.groups_in_flight, (max_batch + d->B - 1) / d->B));
+    d->ws.resize(size_t(d->K));
+    for (auto& w : d->ws) {
+        if ((s = dalloc(&w.r, size_t(L.E_it) * B)) || (s = dalloc(&w.L, size_t(L.n_a) * B)) ||
+            (s = dalloc(&w.lam_a, size_t(L.n_a) * B)) || (s = dalloc(&w.lam1, size_t(L.n_1) * B)) ||
+            (s = dalloc(&w.d1bits, 2 * size_t(L.n_1) * C)) || (s = dalloc(&w.synd_t, size_t(L.m) * C)) ||
+            (s = dalloc(&w.ctl, 16)) || (s = dalloc(&w.iters, B)) || (s = dalloc(&w.conv, B)) ||
+            (s = dalloc(&w.done, 1))) {
+            metldpc_decoder_destroy(d);
+            return s;
+        }
+        cudaMemset(w.d1bits, 0, 2 * size_t(L.n_1) * C * sizeof(uint32_t));
+        cudaMemset(w.ctl, 0, 16 * sizeof(uint32_t));
     }
-    cudaMemset(d->d1bits, 0, 2 * size_t(L.n_1) * C * sizeof(uint32_t));
-    cudaMemset(d->ctl, 0, 16 * sizeof(uint32_t));
+    if (d->K > 1) {
+        d->gs.resize(size_t(d->K));
+        d->join_ev.resize(size_t(d->K));
+        d->fork_ev.resize(1);
+        for (auto& st : d->gs) cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+        for (auto& e : d->join_ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&d->fork_ev[0], cudaEventDisableTiming);
+    }
     const int sms = code->num_sms;
     for (const auto& k : L.classes) {
         // The tiled kernels are specialised for 64-lane groups; other group sizes and the
@@ -343,11 +436,11 @@ metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, cons
             ts = int(std::max(1L, std::min(long(cn_tile_max(D, k.nd)), want)));
             units = ((long(k.count) + ts - 1) / ts) * cn_units_per_tile(D, k.nd);
         }
-        const long full = long(sms) * cn_blocks_per_sm(cfg.rule, D, k.nd);
+        const long full = long(sms) * std::max(1, cn_blocks_per_sm(cfg.rule, D, k.nd) / grid_split(d->K));
         const long need = (units + warps_per_cta - 1) / warps_per_cta;
         d->cn_classes.push_back({D, k.nd, k.begin, k.count, ts, int(std::max(1L, std::min(full, need)))});
     }
-    d->vn_grid = sms * vn_blocks_per_sm();
+    d->vn_grid = sms * std::max(1, vn_blocks_per_sm() / grid_split(d->K));
     d->chk_grid = sms * 4;
     *out = d;
     return METLDPC_OK;
@@ -356,23 +449,28 @@ metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, cons
 void metldpc_decoder_destroy(metldpc_decoder d) {
     if (!d) return;
     cudaSetDevice(d->code->device);
-    dfree(d->r);
-    dfree(d->L);
-    dfree(d->lam_a);
-    dfree(d->lam1);
-    dfree(d->d1bits);
-    dfree(d->synd_t);
-    dfree(d->ctl);
-    dfree(d->iters);
-    dfree(d->conv);
-    dfree(d->done);
-    for (int k = 0; k < 2; ++k) {
-        dfree(d->st_llr[k]);
-        dfree(d->st_synd[k]);
-        dfree(d->st_bits[k]);
-        dfree(d->st_iters[k]);
-        dfree(d->st_conv[k]);
-        dfree(d->st_xnorm[k]);
+    for (auto& w : d->ws) {
+        dfree(w.r);
+        dfree(w.L);
+        dfree(w.lam_a);
+        dfree(w.lam1);
+        dfree(w.d1bits);
+        dfree(w.synd_t);
+        dfree(w.ctl);
+        dfree(w.iters);
+        dfree(w.conv);
+        dfree(w.done);
+    }
+    for (auto st : d->gs) cudaStreamDestroy(st);
+    for (auto e : d->join_ev) cudaEventDestroy(e);
+    for (auto e : d->fork_ev) cudaEventDestroy(e);
+    for (auto& sl : d->st) {
+        dfree(sl.llr);
+        dfree(sl.synd);
+        dfree(sl.bits);
+        dfree(sl.iters);
+        dfree(sl.conv);
+        dfree(sl.xnorm);
     }
     if (d->s_h2d) cudaStreamDestroy(d->s_h2d);
     if (d->s_comp) cudaStreamDestroy(d->s_comp);
@@ -417,10 +515,15 @@ metldpc_status metldpc_decode(metldpc_decoder d, int32_t batch, const float* llr
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const HostLayout& L = d->code->host;
     const size_t W = size_t(L.m + 31) / 32, NW = size_t(L.n + 31) / 32;
-    for (int f0 = 0; f0 < batch; f0 += d->B) {
-        const int nb = std::min(d->B, batch - f0);
-        metldpc_status st = decode_group(d, llr + size_t(f0) * L.n, syndrome + size_t(f0) * W, nb, N,
-                                         bits_out + size_t(f0) * NW, iters_out + f0, conv_out + f0, s);
+    const int groups = (batch + d->B - 1) / d->B;
+    for (int g0 = 0; g0 < groups; g0 += d->K) {
+        std::vector<GroupJob> jobs;
+        for (int k = 0; k < d->K && g0 + k < groups; ++k) {
+            const int f0 = (g0 + k) * d->B;
+            jobs.push_back({k, llr + size_t(f0) * L.n, syndrome + size_t(f0) * W, std::min(d->B, batch - f0),
+                            bits_out + size_t(f0) * NW, iters_out + f0, conv_out + f0, s});
+        }
+        metldpc_status st = decode_round(d, jobs, N, s);
         if (st) return st;
     }
     return METLDPC_OK;
@@ -431,8 +534,9 @@ metldpc_status metldpc_decode(metldpc_decoder d, int32_t batch, const float* llr
 namespace {
 
 // Host-buffer pipeline shared by metldpc_decode_host (LLR input) and
-// metldpc_decode_md_host (MD output input): double-buffered staging; the H2D of group
-// g+1 and the D2H of group g-1 run on their own streams while group g decodes.
+// metldpc_decode_md_host (MD output input).  Groups are decoded in rounds of K (the
+// concurrent workspaces); staging is double-buffered across rounds, so the H2D of round
+// r+1 and the D2H of round r-1 run on their own streams while round r decodes.
 metldpc_status host_pipeline(metldpc_decoder d, int32_t batch, int md, int32_t dim, float snr, const float* in_h,
                              const float* xnorm_h, const uint32_t* synd_h, int32_t max_iter, uint32_t* bits_h,
                              int32_t* iters_h, uint8_t* conv_h) {
@@ -441,15 +545,16 @@ metldpc_status host_pipeline(metldpc_decoder d, int32_t batch, int md, int32_t d
     const HostLayout& L = d->code->host;
     const size_t n = size_t(L.n), W = size_t(L.m + 31) / 32, NW = size_t(L.n + 31) / 32, B = size_t(d->B);
     const size_t nx = md ? n / size_t(dim) : 0;
+    const int K = d->K, S = 2 * K;
     metldpc_status st;
     if (!d->s_comp) {
         CUDA_TRY(cudaStreamCreateWithFlags(&d->s_h2d, cudaStreamNonBlocking));
         CUDA_TRY(cudaStreamCreateWithFlags(&d->s_comp, cudaStreamNonBlocking));
         CUDA_TRY(cudaStreamCreateWithFlags(&d->s_d2h, cudaStreamNonBlocking));
-        for (int k = 0; k < 2; ++k)
-            if ((st = dalloc(&d->st_llr[k], B * n)) || (st = dalloc(&d->st_synd[k], B * W)) ||
-                (st = dalloc(&d->st_bits[k], B * NW)) || (st = dalloc(&d->st_iters[k], B)) ||
-                (st = dalloc(&d->st_conv[k], B)) || (st = dalloc(&d->st_xnorm[k], B * n)))
+        d->st.resize(size_t(S));
+        for (auto& sl : d->st)
+            if ((st = dalloc(&sl.llr, B * n)) || (st = dalloc(&sl.synd, B * W)) || (st = dalloc(&sl.bits, B * NW)) ||
+                (st = dalloc(&sl.iters, B)) || (st = dalloc(&sl.conv, B)) || (st = dalloc(&sl.xnorm, B * n / 8 + B)))
                 return st;
     }
     float c_md = 0.f;
@@ -457,53 +562,68 @@ metldpc_status host_pipeline(metldpc_decoder d, int32_t batch, int md, int32_t d
         const double sd = double(snr);
         c_md = float(2.0 * std::sqrt(sd * (1.0 + sd)));
     }
-    cudaEvent_t in_ready[2], out_ready[2], slot_free[2], out_free[2];
-    for (int k = 0; k < 2; ++k) {
-        cudaEventCreateWithFlags(&in_ready[k], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&out_ready[k], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&slot_free[k], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&out_free[k], cudaEventDisableTiming);
-        cudaEventRecord(slot_free[k], d->s_comp);
-        cudaEventRecord(out_free[k], d->s_d2h);
+    const size_t nslots = static_cast<size_t>(S);
+    std::vector<cudaEvent_t> in_ready(nslots), slot_free(nslots), out_ready(nslots), out_free(nslots);
+    for (int k = 0; k < S; ++k) {
+        cudaEventCreateWithFlags(&in_ready[size_t(k)], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&slot_free[size_t(k)], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&out_ready[size_t(k)], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&out_free[size_t(k)], cudaEventDisableTiming);
+        cudaEventRecord(slot_free[size_t(k)], d->s_comp);
+        cudaEventRecord(out_free[size_t(k)], d->s_d2h);
     }
-    int gi = 0;
+    const int groups = (batch + d->B - 1) / d->B;
     st = METLDPC_OK;
-    for (int f0 = 0; f0 < batch && st == METLDPC_OK; f0 += d->B, ++gi) {
-        const int k = gi & 1;
-        const int nb = std::min(d->B, batch - f0);
-        cudaStreamWaitEvent(d->s_h2d, slot_free[k], 0);
-        cudaMemcpyAsync(d->st_llr[k], in_h + size_t(f0) * n, size_t(nb) * n * sizeof(float), cudaMemcpyHostToDevice,
-                        d->s_h2d);
-        if (md && xnorm_h)
-            cudaMemcpyAsync(d->st_xnorm[k], xnorm_h + size_t(f0) * nx, size_t(nb) * nx * sizeof(float),
-                            cudaMemcpyHostToDevice, d->s_h2d);
-        cudaMemcpyAsync(d->st_synd[k], synd_h + size_t(f0) * W, size_t(nb) * W * sizeof(uint32_t),
-                        cudaMemcpyHostToDevice, d->s_h2d);
-        cudaEventRecord(in_ready[k], d->s_h2d);
-        cudaStreamWaitEvent(d->s_comp, in_ready[k], 0);
-        cudaStreamWaitEvent(d->s_comp, out_free[k], 0);
-        if (md) {   // LLRs in place over the staged v (metldpc_llr_from_md, R13)
-            launch_md_llr(int64_t(nb) * int64_t(n), int(n), dim, c_md, d->st_llr[k], xnorm_h ? d->st_xnorm[k] : nullptr,
-                          d->st_llr[k], d->s_comp);
-            d->prof.launches++;
+    for (int g0 = 0, round = 0; g0 < groups && st == METLDPC_OK; g0 += K, ++round) {
+        std::vector<GroupJob> jobs;
+        std::vector<int> slots;
+        for (int k = 0; k < K && g0 + k < groups; ++k) {
+            const int slot = (round & 1) * K + k;
+            auto& sl = d->st[size_t(slot)];
+            const int f0 = (g0 + k) * d->B, nb = std::min(d->B, batch - f0);
+            // the slot's previous D2H must be done before new inputs overwrite its outputs' neighbours
+            cudaStreamWaitEvent(d->s_h2d, slot_free[size_t(slot)], 0);
+            cudaStreamWaitEvent(d->s_h2d, out_free[size_t(slot)], 0);
+            cudaMemcpyAsync(sl.llr, in_h + size_t(f0) * n, size_t(nb) * n * sizeof(float), cudaMemcpyHostToDevice,
+                            d->s_h2d);
+            if (md && xnorm_h)
+                cudaMemcpyAsync(sl.xnorm, xnorm_h + size_t(f0) * nx, size_t(nb) * nx * sizeof(float),
+                                cudaMemcpyHostToDevice, d->s_h2d);
+            cudaMemcpyAsync(sl.synd, synd_h + size_t(f0) * W, size_t(nb) * W * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                            d->s_h2d);
+            if (md) {   // LLRs in place over the staged v (metldpc_llr_from_md, R13), on the copy stream
+                launch_md_llr(int64_t(nb) * int64_t(n), int(n), dim, c_md, sl.llr, xnorm_h ? sl.xnorm : nullptr, sl.llr,
+                              d->s_h2d);
+                d->prof.launches++;
+            }
+            cudaEventRecord(in_ready[size_t(slot)], d->s_h2d);
+            GroupJob j{k, sl.llr, sl.synd, nb, sl.bits, sl.iters, sl.conv, d->s_comp};
+            j.ready = in_ready[size_t(slot)];
+            j.done = out_ready[size_t(slot)];
+            jobs.push_back(j);
+            slots.push_back(slot);
         }
-        st = decode_group(d, d->st_llr[k], d->st_synd[k], nb, N, d->st_bits[k], d->st_iters[k], d->st_conv[k],
-                          d->s_comp);
-        cudaEventRecord(slot_free[k], d->s_comp);
-        cudaEventRecord(out_ready[k], d->s_comp);
-        cudaStreamWaitEvent(d->s_d2h, out_ready[k], 0);
-        cudaMemcpyAsync(bits_h + size_t(f0) * NW, d->st_bits[k], size_t(nb) * NW * sizeof(uint32_t),
-                        cudaMemcpyDeviceToHost, d->s_d2h);
-        cudaMemcpyAsync(iters_h + f0, d->st_iters[k], size_t(nb) * sizeof(int32_t), cudaMemcpyDeviceToHost, d->s_d2h);
-        cudaMemcpyAsync(conv_h + f0, d->st_conv[k], size_t(nb), cudaMemcpyDeviceToHost, d->s_d2h);
-        cudaEventRecord(out_free[k], d->s_d2h);
+        st = decode_round(d, jobs, N, d->s_comp);
+        for (size_t q = 0; q < jobs.size(); ++q) {
+            const int slot = slots[q];
+            auto& sl = d->st[size_t(slot)];
+            const int f0 = (g0 + int(q)) * d->B, nb = jobs[q].nb;
+            cudaEventRecord(slot_free[size_t(slot)], d->s_comp);
+            cudaStreamWaitEvent(d->s_d2h, out_ready[size_t(slot)], 0);
+            cudaMemcpyAsync(bits_h + size_t(f0) * NW, sl.bits, size_t(nb) * NW * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                            d->s_d2h);
+            cudaMemcpyAsync(iters_h + f0, sl.iters, size_t(nb) * sizeof(int32_t), cudaMemcpyDeviceToHost, d->s_d2h);
+            cudaMemcpyAsync(conv_h + f0, sl.conv, size_t(nb), cudaMemcpyDeviceToHost, d->s_d2h);
+            cudaEventRecord(out_free[size_t(slot)], d->s_d2h);
+        }
     }
     cudaError_t e = cudaStreamSynchronize(d->s_d2h);
-    for (int k = 0; k < 2; ++k) {
-        cudaEventDestroy(in_ready[k]);
-        cudaEventDestroy(out_ready[k]);
-        cudaEventDestroy(slot_free[k]);
-        cudaEventDestroy(out_free[k]);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(d->s_comp);
+    for (int k = 0; k < S; ++k) {
+        cudaEventDestroy(in_ready[size_t(k)]);
+        cudaEventDestroy(slot_free[size_t(k)]);
+        cudaEventDestroy(out_ready[size_t(k)]);
+        cudaEventDestroy(out_free[size_t(k)]);
     }
     if (st) return st;
     if (e != cudaSuccess) return fail(METLDPC_ECUDA, std::string("host pipeline: ") + cudaGetErrorString(e));
@@ -561,12 +681,12 @@ metldpc_status metldpc_debug_dump(metldpc_decoder d, int32_t lane, float* r_out,
     const HostLayout& L = d->code->host;
     if (r_out && L.E_it) {   // device order (relabelled CNs) -> canonical active-edge CSR order
         std::vector<float> tmp(size_t(L.E_it));
-        CUDA_TRY(cudaMemcpy2D(tmp.data(), sizeof(float), d->r + lane, size_t(d->B) * sizeof(float), sizeof(float),
+        CUDA_TRY(cudaMemcpy2D(tmp.data(), sizeof(float), d->ws[size_t(d->last_ws)].r + lane, size_t(d->B) * sizeof(float), sizeof(float),
                               size_t(L.E_it), cudaMemcpyDeviceToHost));
         for (int64_t t = 0; t < L.E_it; ++t) r_out[L.perm_r[size_t(t)]] = tmp[size_t(t)];
     }
     if (L_out && L.n_a)
-        CUDA_TRY(cudaMemcpy2D(L_out, sizeof(float), d->L + lane, size_t(d->B) * sizeof(float), sizeof(float),
+        CUDA_TRY(cudaMemcpy2D(L_out, sizeof(float), d->ws[size_t(d->last_ws)].L + lane, size_t(d->B) * sizeof(float), sizeof(float),
                               size_t(L.n_a), cudaMemcpyDeviceToHost));
     return METLDPC_OK;
 }

@@ -215,10 +215,14 @@ std::vector<float> phi_device_table(int rule) {
     std::vector<float> base(size_t(nb) * per);
     if (ex) phi_table_exact(base.data());
     else phi_table_lut(base.data());
+    // coefficients pre-scaled by 2^(J q) (exact: power-of-two scaling of an fp32 value), so the
+    // kernel evaluates the polynomial in t / 2^J -- bit-identical results (kernels.cu phi_dev)
+    const int J = ex ? kPhiJExact : kPhiJLut;
     std::vector<float> dev(size_t(nb + 1) * kPhiCopies * per, 0.0f);   // last bin: zero sentinel
     for (int b = 0; b < nb; ++b)
         for (int k = 0; k < kPhiCopies; ++k)
-            for (int q = 0; q < per; ++q) dev[(size_t(b) * kPhiCopies + k) * per + q] = base[size_t(b) * per + q];
+            for (int q = 0; q < per; ++q)
+                dev[(size_t(b) * kPhiCopies + k) * per + q] = std::ldexp(base[size_t(b) * per + q], J * q);
     return dev;
 }
 

@@ -46,22 +46,25 @@ struct PhiT<METLDPC_RULE_PHI_LUT> {    // linear, 32 bins per binade
 // phi(y), y >= 0, exactly as DESIGN.md N2: clamping the bit pattern to [2^-44, 2^6]
 // reproduces both out-of-range rules with no selects (u = 2^-44: bin 0, t = 0, c0 =
 // (float)phi(2^-44) = PHI_TOP; u = 2^6: the zero sentinel bin, +0).  The bin's byte
-// offset is (u >> (23 - J)) * STRIDE = (u >> 12) with the low bits cleared, and
-// t = (u mod 2^(23-J)) / 2^(23-J) is formed exactly as (1 + m) - 1 from the mantissa bits.
-// tabk = table base + (lane & 7) * ENTRY - BIAS (see phi_tab_lane).
+// offset is (u >> (23 - J)) * STRIDE = (u with the low 23-J bits cleared) >> 12.
+// The device table stores the coefficients pre-scaled by powers of two, c_k * 2^(J k),
+// and the polynomial runs in ts = t / 2^J = bits(1.0 | low mantissa bits) - 1 (exact):
+// scaling by a power of two commutes with rounding, so every Horner intermediate is the
+// oracle's times 2^(J k) and the result is bit-identical to N2 as written.
 template <int RULE>
 __device__ __forceinline__ float phi_dev(const char* tabk, float y) {
     using P = PhiT<RULE>;
     static_assert(P::STRIDE == (1 << (11 - P::J)), "(u >> (23 - J)) * STRIDE == (u & ~low) >> 12");
+    constexpr uint32_t LOW = (1u << (23 - P::J)) - 1u;
     const uint32_t u = min(max(__float_as_uint(y), kPhiLoBits), kPhiHiBits);
-    const char* e = tabk + ((u & ~((1u << (23 - P::J)) - 1u)) >> 12);
-    const float t = __fsub_rn(__uint_as_float(((u << P::J) & 0x007FFFFFu) | 0x3F800000u), 1.0f);
+    const char* e = tabk + ((u & ~LOW) >> 12);
+    const float ts = __fsub_rn(__uint_as_float((u & LOW) | 0x3F800000u), 1.0f);
     if constexpr (RULE == METLDPC_RULE_EXACT) {
         const float4 c = *reinterpret_cast<const float4*>(e);
-        return __fmaf_rn(__fmaf_rn(__fmaf_rn(c.w, t, c.z), t, c.y), t, c.x);
+        return __fmaf_rn(__fmaf_rn(__fmaf_rn(c.w, ts, c.z), ts, c.y), ts, c.x);
     } else {
         const float2 c = *reinterpret_cast<const float2*>(e);
-        return __fmaf_rn(c.y, t, c.x);
+        return __fmaf_rn(c.y, ts, c.x);
     }
 }
 
@@ -103,7 +106,7 @@ __device__ __forceinline__ uint32_t cn_lane(const char* tabk, const float (&Lv)[
 #pragma unroll
     for (int s = 0; s < NA; ++s) {
         const float x = __fsub_rn(Lv[s], ro[s]);         // extrinsic q = L - r (R10)
-        chk ^= uint32_t(Lv[s] < 0.0f);                    // c_v^{l-1} (a decision: comparison)
+        chk ^= __float_as_uint(__fadd_rn(Lv[s], 0.0f)) >> 31;   // c_v^{l-1} = [L < 0] (-0 + 0 = +0)
         xb[s] = __float_as_uint(__fadd_rn(x, 0.0f));
         par ^= xb[s];
         p[s] = phi_dev<RULE>(tabk, fabsf(x));
@@ -113,13 +116,16 @@ __device__ __forceinline__ uint32_t cn_lane(const char* tabk, const float (&Lv)[
         par ^= xb[NA];
         p[NA] = phi_dev<RULE>(tabk, fabsf(lam));
     }
-    float acc = 0.0f;
+    // P_0 = 0, P_{k+1} = P_k + p_k; Q_{D-1} = 0, Q_k = Q_{k+1} + p_{k+1}; S_k = P_k + Q_k.
+    // The additions with an exact +0 operand are skipped: p, P, Q >= +0, so 0 + v = v.
+    P[0] = 0.0f;
+    if constexpr (D > 1) P[1] = p[0];
 #pragma unroll
-    for (int s = 0; s < D; ++s) { P[s] = acc; acc = __fadd_rn(acc, p[s]); }
+    for (int s = 2; s < D; ++s) P[s] = __fadd_rn(P[s - 1], p[s - 1]);
     float Q = 0.0f;
 #pragma unroll
     for (int s = D - 1; s >= 0; --s) {
-        const float S = __fadd_rn(P[s], Q);
+        const float S = (s == D - 1) ? P[s] : (s == 0 ? Q : __fadd_rn(P[s], Q));
         const float mag = fminf(phi_dev<RULE>(tabk, S), kRMax);
         const float o = __uint_as_float(__float_as_uint(mag) | ((par ^ xb[s]) & 0x80000000u));
         if (s < NA) {
@@ -138,8 +144,8 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 }
 
 #ifndef METLDPC_CN_PF
-#define METLDPC_CN_PF 4     // CNs of look-ahead for the r / lambda L2 prefetch
-#endif
+#define METLDPC_CN_PF 0     // CNs of look-ahead for an r / lambda L2 prefetch (0: off; measured
+#endif                      // slower at 4 and 8 -- the kernel is issue-bound, not DRAM-latency-bound)
 
 // One degree class (CN labels [begin, begin + count), NA active + ND <= 1 degree-1 slots)
 // for 64-lane groups.  Work unit = a tile of ts consecutive CNs owned by one warp; for
@@ -193,7 +199,7 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_tile(CodeDev cd, Group g, 
                 for (int e = lane; e < nt * NA; e += 32) s_idx[e] = __ldg(cd.a_vn + A0 + e) * 64;
                 __syncwarp();
             }
-            if (lane < min(nt, METLDPC_CN_PF)) {    // look-ahead for the first CNs of the tile
+            if (METLDPC_CN_PF > 0 && lane < min(nt, METLDPC_CN_PF)) {   // look-ahead for the first CNs
                 if constexpr (NA > 0) prefetch_l2(g.r + size_t(a_l) * 64, NA * 256);
                 if constexpr (ND > 0) prefetch_l2(g.lam1 + size_t(d_l) * 64, 256);
             }
@@ -201,7 +207,7 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_tile(CodeDev cd, Group g, 
                 const int ab = __shfl_sync(FULL, a_l, i);
                 const int q0 = __shfl_sync(FULL, d_l, i);
                 const uint32_t swx = __shfl_sync(FULL, sw_l.x, i), swy = __shfl_sync(FULL, sw_l.y, i);
-                {
+                if (METLDPC_CN_PF > 0) {
                     const int ip = i + METLDPC_CN_PF;    // keep the DRAM stream PF CNs ahead
                     const int abp = __shfl_sync(FULL, a_l, ip & 31), q0p = __shfl_sync(FULL, d_l, ip & 31);
                     if (lane == 0 && ip < nt) {

@@ -40,9 +40,9 @@ def _llr_oracle(fr):
     return np.stack([bp.llr_from_md_f32(fr["v"][i], fr["xnorm"][i], fr["snr"][i]) for i in range(len(fr["v"]))])
 
 
-def _gpu_decode(code_h, llr, synd, rule, max_iter, et=True, lanes=64, max_batch=None):
+def _gpu_decode(code_h, llr, synd, rule, max_iter, et=True, lanes=64, max_batch=None, groups=None):
     dec = B.Decoder(code_h, max_batch or llr.shape[0], rule=rule, max_iter=max_iter, early_term=et,
-                    lanes_per_group=lanes)
+                    lanes_per_group=lanes, groups_in_flight=groups)
     bits, iters, conv = dec.decode(torch.from_numpy(llr).cuda(), torch.from_numpy(synd.view(np.int32)).cuda())
     torch.cuda.synchronize()
     return dec, bits.cpu().numpy().view(np.uint32), iters.cpu().numpy(), conv.cpu().numpy()
@@ -125,17 +125,18 @@ def test_batch_lane_and_group_invariance(c1, et):
     fr = _frames(code, [(0.161, 30), (0.3, 40), (0.6, 30)])
     llr = _llr_oracle(fr)
     ref = None
-    for lanes in (32, 64, 128):
+    for lanes, groups in ((32, 1), (64, 1), (64, 2), (64, 3), (128, 2)):
         for order in ("fwd", "rev"):
             idx = np.arange(len(llr)) if order == "fwd" else np.arange(len(llr))[::-1].copy()
-            _, bits, iters, conv = _gpu_decode(h, llr[idx], fr["synd"][idx], B.RULE_EXACT, 60, et=et, lanes=lanes)
+            _, bits, iters, conv = _gpu_decode(h, llr[idx], fr["synd"][idx], B.RULE_EXACT, 60, et=et, lanes=lanes,
+                                               groups=groups)
             inv = np.argsort(idx)
             res = (bits[inv], iters[inv], conv[inv])
             if ref is None:
                 ref = res
             else:
                 for a, b in zip(ref, res):
-                    assert np.array_equal(a, b), (lanes, order)
+                    assert np.array_equal(a, b), (lanes, groups, order)
     # single-frame batches agree too
     for i in (0, 45, 99):
         _, bits, iters, conv = _gpu_decode(h, llr[i:i + 1], fr["synd"][i:i + 1], B.RULE_EXACT, 60, et=et)
@@ -148,8 +149,8 @@ def test_ragged_batch_max_batch_and_host_path(c1):
     code, h = c1
     fr = _frames(code, [(0.2, 37), (0.4, 40)])
     llr = _llr_oracle(fr)
-    _, bits, iters, conv = _gpu_decode(h, llr, fr["synd"], B.RULE_PHI_LUT, 50, max_batch=200)
-    dec = B.Decoder(h, 200, rule=B.RULE_PHI_LUT, max_iter=50)
+    _, bits, iters, conv = _gpu_decode(h, llr, fr["synd"], B.RULE_PHI_LUT, 50, max_batch=200, groups=1)
+    dec = B.Decoder(h, 200, rule=B.RULE_PHI_LUT, max_iter=50, groups_in_flight=2)
     hb, hi, hc = dec.decode_host(np.ascontiguousarray(llr), np.ascontiguousarray(fr["synd"]))
     assert np.array_equal(hb, bits) and np.array_equal(hi, iters) and np.array_equal(hc, conv)
     for i in (0, 36, 76):
