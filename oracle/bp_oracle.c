@@ -24,8 +24,9 @@
  *       forward sums P_0 = 0, P_{k+1} = P_k + p_k; backward sums Q_{d-1} = 0,
  *       Q_k = Q_{k+1} + p_{k+1}; S_k = P_k + Q_k;
  *       o_k = (-1)^(XOR_{k'!=k} n_k' XOR s_j) * min(phi(S_k), R_MAX).
- *   VN phase (Eq. 4/5): L_i = lambda_i + sum of r over C_i, a left fold in
- *       the caller's CSC slot order.
+ *   VN phase (Eq. 4/5): L_i = lambda_i + sum of r over C_i -- in fp64 (M2) a left
+ *       fold in the caller's CSC slot order; in fp32 (M3) an exact fixed-point sum
+ *       with 2^-17 resolution (N3, see vn_phase32).
  *   Decisions (Step 5, Eq. 5): c_i = [L_i < 0] for active VNs,
  *       c_v = [lambda_v + rho_v < 0] for degree-1 VNs (rho = their CN output);
  *       a tie (exact zero) gives 0 -- "if q_i^l > 1, c_i = 1".
@@ -284,12 +285,22 @@ static void cn_phase32(const graph_t* g, int rule, const float* lam, const uint3
     free(x); free(p); free(P); free(Q); free(slot_e);
 }
 
+/* DESIGN.md N3 (fp32 replay): the sum of Eq. (4)/(5) over C_i is taken exactly in
+ * fixed point -- each message rounded to the nearest multiple of 2^-17 (ties to even),
+ * the integers added exactly, the total converted to fp32 (round to nearest) and scaled:
+ * L_i = lambda_i + (float)(sum_k rint(2^17 r_k)) * 2^-17.  An exact integer sum has no
+ * order, so the result is independent of the order the messages arrive in. */
+#define VN_FIX_BITS 17
 static void vn_phase32(const graph_t* g, const float* lam, const float* r_new, float* L_new) {
     for (int a = 0; a < g->n_a; ++a) {
         int v = g->act_vn[a];
-        float acc = lam[v];
-        for (int64_t k = g->vn_ptr[v]; k < g->vn_ptr[v + 1]; ++k) acc = acc + r_new[g->act_id[g->vn_edge[k]]];
-        L_new[a] = acc;
+        int64_t acc = 0;
+        for (int64_t k = g->vn_ptr[v]; k < g->vn_ptr[v + 1]; ++k) {
+            float scaled = r_new[g->act_id[g->vn_edge[k]]] * (float)(1 << VN_FIX_BITS);   /* exact */
+            acc += (int64_t)rintf(scaled);
+        }
+        float sum = (float)acc * (1.0f / (float)(1 << VN_FIX_BITS));
+        L_new[a] = lam[v] + sum;
     }
 }
 

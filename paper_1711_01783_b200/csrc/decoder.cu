@@ -245,7 +245,7 @@ void group_iter(metldpc_decoder d, const GroupJob& j, int l) {
         d->prof.launches++;
     }
     e = ev_begin(d, 1, j.s);
-    launch_vn(cd, g, d->vn_grid, j.s);
+    launch_finish(cd, g, d->vn_grid, j.s);
     ev_end(d, e, j.s);
     d->prof.vn_launches++;
     d->prof.launches++;
@@ -403,7 +403,7 @@ metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, cons
     d->K = std::max(1, std::min(cfg.groups_in_flight, (max_batch + d->B - 1) / d->B));
     d->ws.resize(size_t(d->K));
     for (auto& w : d->ws) {
-        if ((s = dalloc(&w.r, size_t(L.E_it) * B)) || (s = dalloc(&w.L, size_t(L.n_a) * B)) ||
+        if ((s = dalloc(&w.r, size_t(L.E_it) * B)) || (s = dalloc(&w.L, 2 * size_t(L.n_a) * B)) ||
             (s = dalloc(&w.lam_a, size_t(L.n_a) * B)) || (s = dalloc(&w.lam1, size_t(L.n_1) * B)) ||
             (s = dalloc(&w.d1bits, 2 * size_t(L.n_1) * C)) || (s = dalloc(&w.synd_t, size_t(L.m) * C)) ||
             (s = dalloc(&w.ctl, 16)) || (s = dalloc(&w.iters, B)) || (s = dalloc(&w.conv, B)) ||
@@ -440,7 +440,7 @@ metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, cons
         const long need = (units + warps_per_cta - 1) / warps_per_cta;
         d->cn_classes.push_back({D, k.nd, k.begin, k.count, ts, int(std::max(1L, std::min(full, need)))});
     }
-    d->vn_grid = sms * std::max(1, vn_blocks_per_sm() / grid_split(d->K));
+    d->vn_grid = sms * std::max(1, finish_blocks_per_sm() / grid_split(d->K));
     d->chk_grid = sms * 4;
     *out = d;
     return METLDPC_OK;
@@ -686,7 +686,7 @@ metldpc_status metldpc_debug_dump(metldpc_decoder d, int32_t lane, float* r_out,
         for (int64_t t = 0; t < L.E_it; ++t) r_out[L.perm_r[size_t(t)]] = tmp[size_t(t)];
     }
     if (L_out && L.n_a)
-        CUDA_TRY(cudaMemcpy2D(L_out, sizeof(float), d->ws[size_t(d->last_ws)].L + lane, size_t(d->B) * sizeof(float), sizeof(float),
+        CUDA_TRY(cudaMemcpy2D(L_out, sizeof(float), d->ws[size_t(d->last_ws)].L + lane, 2 * size_t(d->B) * sizeof(float), sizeof(float),
                               size_t(L.n_a), cudaMemcpyDeviceToHost));
     return METLDPC_OK;
 }

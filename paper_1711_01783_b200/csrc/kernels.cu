@@ -94,10 +94,18 @@ constexpr int kCnThreads = 512;   // 2 CTAs x 16 warps per SM (the replicated ta
 // slot): Eqs. (2)-(3) in sign/phi form with the syndrome sign (R1).
 // Returns the syndrome-test bit (N4) of iteration l-1; writes r for active slots and
 // the degree-1 decision bit.
+// Fixed-point VN-sum term of a message (N3): bits(fmaf(o, 2^17, 1.5 * 2^23)) =
+// 0x4B400000 + rint(2^17 o) exactly for |2^17 o| < 2^22 (|o| <= 30); the finish kernel
+// removes the 0x4B400000 bias (degree times, modulo 2^32).
+__device__ __forceinline__ uint32_t vn_fix(float o) {
+    return __float_as_uint(__fmaf_rn(o, 131072.0f, 12582912.0f));
+}
+
 template <int RULE, int NA, int ND>
 __device__ __forceinline__ uint32_t cn_lane(const char* tabk, const float (&Lv)[NA > 0 ? NA : 1],
                                             const float (&ro)[NA > 0 ? NA : 1], float lam, uint32_t sbit,
-                                            uint32_t d1prev, float* pr, bool act, uint32_t& d1bit) {
+                                            uint32_t d1prev, float* pr, float* pla, const int (&offs)[NA > 0 ? NA : 1],
+                                            const int* idx, bool act, uint32_t& d1bit) {
     constexpr int D = NA + ND;
     float p[D], P[D];
     uint32_t xb[D];     // bits of x + 0.0f: sign bit = [x < 0] exactly (-0 + 0 = +0), N1 / R2
@@ -129,7 +137,12 @@ __device__ __forceinline__ uint32_t cn_lane(const char* tabk, const float (&Lv)[
         const float mag = fminf(phi_dev<RULE>(tabk, S), kRMax);
         const float o = __uint_as_float(__float_as_uint(mag) | ((par ^ xb[s]) & 0x80000000u));
         if (s < NA) {
-            if (act) __stcs(pr + s * 64, o);
+            if (act) {
+                __stcs(pr + s * 64, o);
+                // VN sum (Eq. 4); row offsets from registers for small NA, from shared memory otherwise
+                const int ro_s = (NA <= 4) ? offs[s] : idx[s];
+                atomicAdd(reinterpret_cast<unsigned int*>(pla + ro_s + 64), vn_fix(o));
+            }
         } else {
             d1bit = uint32_t(__fadd_rn(lam, o) < 0.0f);   // Step 5 for VN_b
         }
@@ -154,9 +167,12 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 // The tile's metadata is one coalesced load per array, its active-edge VN indices
 // (pre-scaled to row offsets) are staged in shared memory, and the r / lambda rows of
 // the CN PF positions ahead are prefetched into L2 by the TMA unit.
+template <int NA>
+__host__ __device__ constexpr int cn_tile_min_blocks() { return NA <= 4 ? 2 : 1; }   // NA > 4: 128 registers
+
 template <int RULE, int NA, int ND>
-__global__ void __launch_bounds__(kCnThreads, 2) k_cn_tile(CodeDev cd, Group g, CnCtl k, int begin, int count,
-                                                           int ts) {
+__global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_tile(CodeDev cd, Group g, CnCtl k,
+                                                                                  int begin, int count, int ts) {
     using PT = PhiT<RULE>;
     constexpr int LPT = (NA <= 4) ? 2 : 1;     // lanes per thread
     constexpr int UPT = 2 / LPT;               // units per tile
@@ -196,7 +212,7 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_tile(CodeDev cd, Group g, 
             const int A0 = __shfl_sync(FULL, a_l, 0);
             if constexpr (NA > 0) {
                 __syncwarp();
-                for (int e = lane; e < nt * NA; e += 32) s_idx[e] = __ldg(cd.a_vn + A0 + e) * 64;
+                for (int e = lane; e < nt * NA; e += 32) s_idx[e] = __ldg(cd.a_vn + A0 + e) * 128;
                 __syncwarp();
             }
             if (METLDPC_CN_PF > 0 && lane < min(nt, METLDPC_CN_PF)) {   // look-ahead for the first CNs
@@ -216,13 +232,15 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_tile(CodeDev cd, Group g, 
                     }
                 }
                 const int* idx = s_idx + (ab - A0);
-                const float* pL = g.L + (c0 * 32 + lane);
+                float* pL = g.L + (c0 * 32 + lane);
                 float* pr = g.r + (size_t(ab) * 64 + c0 * 32 + lane);
                 float Lv[LPT][NAS], ro[LPT][NAS], lam[LPT];
+                int offs[NAS];
                 uint32_t w[LPT];
 #pragma unroll
                 for (int s = 0; s < NA; ++s) {
                     const int o = idx[s];
+                    if constexpr (NA <= 4) offs[s] = o;
 #pragma unroll
                     for (int h = 0; h < LPT; ++h) {
                         Lv[h][s] = __ldg(pL + o + h * 32);
@@ -247,7 +265,8 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_tile(CodeDev cd, Group g, 
                     w[h] = (((c ? wv.y : wv.x) >> lane) & 1u);
                     const bool act = (((c ? am1 : am0) >> lane) & 1u) != 0u;
                     b[h] = 0;
-                    chk[h] = cn_lane<RULE, NA, ND>(tabk, Lv[h], ro[h], lam[h], sbit, w[h], pr + h * 32, act, b[h]);
+                    chk[h] = cn_lane<RULE, NA, ND>(tabk, Lv[h], ro[h], lam[h], sbit, w[h], pr + h * 32, pL + h * 32, offs,
+                                                   idx, act, b[h]);
                 }
 #pragma unroll
                 for (int h = 0; h < LPT; ++h) {
@@ -312,7 +331,7 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group 
             float x;
             if (s < na) {
                 const int v = __shfl_sync(FULL, idx, s);
-                const float Lv = __ldg(g.L + size_t(v) * g.B + off);
+                const float Lv = __ldg(g.L + size_t(v) * 2 * g.B + off);
                 const float ro = k.first ? 0.0f : __ldcs(g.r + size_t(ab + s) * g.B + off);
                 x = __fsub_rn(Lv, ro);
                 chk ^= uint32_t(Lv < 0.0f);
@@ -339,7 +358,11 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group 
             const float mag = fminf(phi_dev<RULE>(tabk, S), kRMax);
             const float o = __uint_as_float(__float_as_uint(mag) | ((par ^ ((negmask >> s) & 1u)) << 31));
             if (s < na) {
-                if (act) __stcs(g.r + size_t(ab + s) * g.B + off, o);
+                const int v = __shfl_sync(FULL, idx, s);      // whole warp: lane s may be an idle lane
+                if (act) {
+                    __stcs(g.r + size_t(ab + s) * g.B + off, o);
+                    atomicAdd(reinterpret_cast<unsigned int*>(g.L + size_t(v) * 2 * g.B + g.B + off), vn_fix(o));
+                }
             } else {
                 const uint32_t bal = __ballot_sync(FULL, __fadd_rn(xs[s], o) < 0.0f);
                 if (lane == 0) {
@@ -372,7 +395,7 @@ __global__ void __launch_bounds__(256) k_check(CodeDev cd, Group g, int par) {
         const int ab = __ldg(cd.cn_aptr + j), ae = __ldg(cd.cn_aptr + j + 1);
         const int db = __ldg(cd.cn_dptr + j), de = __ldg(cd.cn_dptr + j + 1);
         uint32_t chk = (__ldg(g.synd_t + size_t(j) * g.C + c) >> lane) & 1u;
-        for (int t = ab; t < ae; ++t) chk ^= uint32_t(__ldg(g.L + size_t(__ldg(cd.a_vn + t)) * g.B + off) < 0.0f);
+        for (int t = ab; t < ae; ++t) chk ^= uint32_t(__ldg(g.L + size_t(__ldg(cd.a_vn + t)) * 2 * g.B + off) < 0.0f);
         for (int q = db; q < de; ++q) chk ^= (__ldg(g.d1bits + (size_t(par) * cd.n_1 + q) * g.C + c) >> lane) & 1u;
         const uint32_t mm = __ballot_sync(FULL, chk) & amask;
         if (mm && lane == 0) atomicOr(&s_unsat[c], mm);
@@ -383,97 +406,39 @@ __global__ void __launch_bounds__(256) k_check(CodeDev cd, Group g, int par) {
 
 // ------------------------------------------------------------------ variable-node update (a3)
 
-// L_a = lambda_a + sum of r over C_a, left fold in the caller's CSC slot order (Eq. 4/5, N3).
-__global__ void __launch_bounds__(256) k_vn_update(CodeDev cd, Group g) {
+// Eq. (4)/(5), N3: the CN pass has accumulated, per active VN a and lane b, the
+// exact fixed-point sum sum_k bits(fmaf(r_k, 2^17, 1.5 * 2^23)) (mod 2^32); remove the
+// degree x 0x4B400000 bias, L = lambda + (float)sum * 2^-17 for lanes still iterating,
+// and clear the accumulator for the next iteration.  Four lanes per thread (128-bit).
+__global__ void __launch_bounds__(256) k_finish(CodeDev cd, Group g) {
     __shared__ uint32_t s_act[4];
     if (*reinterpret_cast<volatile int*>(g.done)) return;
     if (threadIdx.x < g.C) s_act[threadIdx.x] = g.act[threadIdx.x];
     __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int wpb = blockDim.x >> 5;
-    const int lc = __ffs(g.C) - 1;
-    const int B = g.B;
-    const long total = long(cd.n_a) << lc;
-    for (long item = long(blockIdx.x) * wpb + (threadIdx.x >> 5); item < total; item += long(gridDim.x) * wpb) {
-        const int a = int(item >> lc), c = int(item & (g.C - 1));
-        const uint32_t amask = s_act[c];
-        if (!amask) continue;
-        const size_t off = size_t(c) * 32 + lane;
-        const int vb = __ldg(cd.vn_aptr + a), ve = __ldg(cd.vn_aptr + a + 1);
-        float acc = __ldg(g.lam_a + size_t(a) * B + off);
-        for (int base = vb; base < ve; base += 32) {
-            const int cnt = min(32, ve - base);
-            const int eid = (lane < cnt) ? __ldg(cd.vn_aedge + base + lane) : 0;
-            int s = 0;
-            for (; s + 8 <= cnt; s += 8) {
-                float v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = __ldcs(g.r + size_t(__shfl_sync(FULL, eid, s + u)) * B + off);
-#pragma unroll
-                for (int u = 0; u < 8; ++u) acc = __fadd_rn(acc, v[u]);
-            }
-            for (; s < cnt; ++s) acc = __fadd_rn(acc, __ldcs(g.r + size_t(__shfl_sync(FULL, eid, s)) * B + off));
-        }
-        if ((amask >> lane) & 1u) g.L[size_t(a) * B + off] = acc;
+    const int qpr = g.B >> 2;                           // float4 quads per row half
+    const long total = long(cd.n_a) * qpr;
+    for (long t = long(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += long(gridDim.x) * blockDim.x) {
+        const int a = int(t / qpr), q = int(t - long(a) * qpr);
+        const int deg = __ldg(cd.vn_aptr + a + 1) - __ldg(cd.vn_aptr + a);
+        const uint32_t bias = uint32_t(deg) * 0x4B400000u;
+        float4* Lrow = reinterpret_cast<float4*>(g.L + size_t(a) * 2 * g.B);
+        uint4* Arow = reinterpret_cast<uint4*>(g.L + size_t(a) * 2 * g.B + g.B);
+        const uint4 acc = Arow[q];
+        const float4 lam = __ldg(reinterpret_cast<const float4*>(g.lam_a + size_t(a) * g.B) + q);
+        const int b0 = q * 4;
+        const uint32_t m = (s_act[b0 >> 5] >> (b0 & 31)) & 0xFu;
+        float4 L = Lrow[q];
+        const float sc = 1.0f / 131072.0f;
+        if (m & 1u) L.x = __fadd_rn(lam.x, __fmul_rn(__int2float_rn(int(acc.x - bias)), sc));
+        if (m & 2u) L.y = __fadd_rn(lam.y, __fmul_rn(__int2float_rn(int(acc.y - bias)), sc));
+        if (m & 4u) L.z = __fadd_rn(lam.z, __fmul_rn(__int2float_rn(int(acc.z - bias)), sc));
+        if (m & 8u) L.w = __fadd_rn(lam.w, __fmul_rn(__int2float_rn(int(acc.w - bias)), sc));
+        if (m) Lrow[q] = L;
+        Arow[q] = make_uint4(0u, 0u, 0u, 0u);
     }
 }
 
-// ------------------------------------------------------------------ 64-lane tiled VN update / check
-
-// Eq. (4)/(5), N3 for 64-lane groups: one warp per tile of 8 consecutive active VNs,
-// both 32-lane chunks per thread; the tile's column offsets are one coalesced load, each
-// column's CSC edge ids another (pre-scaled to row offsets), gathers batched 8 deep.
-__global__ void __launch_bounds__(256) k_vn_tile64(CodeDev cd, Group g) {
-    __shared__ uint32_t s_act[2];
-    if (*reinterpret_cast<volatile int*>(g.done)) return;
-    if (threadIdx.x < 2) s_act[threadIdx.x] = g.act[threadIdx.x];
-    __syncthreads();
-    const uint32_t am0 = s_act[0], am1 = s_act[1];
-    if (!(am0 | am1)) return;
-    const int lane = threadIdx.x & 31;
-    const bool act0 = (am0 >> lane) & 1u, act1 = (am1 >> lane) & 1u;
-    const int wpb = blockDim.x >> 5;
-    constexpr int TV = 8;     // VNs per warp tile (keeps every warp busy: n_a / 8 tiles)
-    const int ntiles = (cd.n_a + TV - 1) / TV;
-    const float* rl = g.r + lane;
-    for (int tile = blockIdx.x * wpb + (threadIdx.x >> 5); tile < ntiles; tile += gridDim.x * wpb) {
-        const int a0 = tile * TV;
-        const int nt = min(TV, cd.n_a - a0);
-        const int vb_l = lane < nt ? __ldg(cd.vn_aptr + a0 + lane) : 0;
-        const int ve_l = lane < nt ? __ldg(cd.vn_aptr + a0 + lane + 1) : 0;
-        for (int i = 0; i < nt; ++i) {
-            const int vb = __shfl_sync(FULL, vb_l, i), ve = __shfl_sync(FULL, ve_l, i);
-            const size_t row = size_t(a0 + i) * 64 + lane;
-            float acc0 = __ldg(g.lam_a + row), acc1 = __ldg(g.lam_a + row + 32);
-            for (int base = vb; base < ve; base += 32) {
-                const int cnt = min(32, ve - base);
-                const int eid = (lane < cnt) ? __ldg(cd.vn_aedge + base + lane) * 64 : 0;
-                int s = 0;
-                for (; s + 8 <= cnt; s += 8) {
-                    float v0[8], v1[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int e = __shfl_sync(FULL, eid, s + u);
-                        v0[u] = __ldcs(rl + e);
-                        v1[u] = __ldcs(rl + e + 32);
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        acc0 = __fadd_rn(acc0, v0[u]);
-                        acc1 = __fadd_rn(acc1, v1[u]);
-                    }
-                }
-                for (; s < cnt; ++s) {
-                    const int e = __shfl_sync(FULL, eid, s);
-                    acc0 = __fadd_rn(acc0, __ldcs(rl + e));
-                    acc1 = __fadd_rn(acc1, __ldcs(rl + e + 32));
-                }
-            }
-            if (act0) g.L[row] = acc0;
-            if (act1) g.L[row + 32] = acc1;
-        }
-    }
-}
+// ------------------------------------------------------------------ 64-lane tiled syndrome check
 
 // Syndrome test of iteration l = N (N4) for 64-lane groups: warp per tile of 32 CNs.
 __global__ void __launch_bounds__(256) k_check64(CodeDev cd, Group g, int par) {
@@ -499,7 +464,7 @@ __global__ void __launch_bounds__(256) k_check64(CodeDev cd, Group g, int par) {
                 const int db = __shfl_sync(FULL, d_l, i), nd = __shfl_sync(FULL, de_l, i) - db;
                 uint32_t c0 = (__shfl_sync(FULL, sw_l.x, i) >> lane) & 1u;
                 uint32_t c1 = (__shfl_sync(FULL, sw_l.y, i) >> lane) & 1u;
-                const int idx = (lane < na) ? __ldg(cd.a_vn + ab + lane) * 64 : 0;
+                const int idx = (lane < na) ? __ldg(cd.a_vn + ab + lane) * 128 : 0;
                 for (int s = 0; s < na; ++s) {
                     const int o = __shfl_sync(FULL, idx, s);
                     c0 ^= uint32_t(__ldg(Ll + o) < 0.0f);
@@ -574,7 +539,8 @@ __global__ void __launch_bounds__(256) k_scatter(CodeDev cd, Group g, const floa
         const int v = __ldg(cd.vmap + i);
         if (v >= 0) {
             g.lam_a[size_t(v) * g.B + off] = val;
-            g.L[size_t(v) * g.B + off] = val;                       // L^0 = lambda (Step 2)
+            g.L[size_t(v) * 2 * g.B + off] = val;                    // L^0 = lambda (Step 2)
+            g.L[size_t(v) * 2 * g.B + g.B + off] = 0.0f;             // empty VN-sum accumulator
         } else {
             g.lam1[size_t(~v) * g.B + off] = val;
         }
@@ -650,7 +616,7 @@ __global__ void __launch_bounds__(256) k_finalize(CodeDev cd, Group g, int nb, u
         const int v = __ldg(cd.vmap + i);
         uint32_t b;
         if (v >= 0) {
-            b = g.L[size_t(v) * g.B + off] < 0.0f;
+            b = g.L[size_t(v) * 2 * g.B + off] < 0.0f;
         } else {
             const uint32_t w0 = g.d1bits[(size_t(0) * cd.n_1 + ~v) * g.C + c];
             const uint32_t w1 = g.d1bits[(size_t(1) * cd.n_1 + ~v) * g.C + c];
@@ -753,11 +719,9 @@ int cn_blocks_per_sm(int rule, int D, int nd) {
     return nb > 0 ? nb : 1;
 }
 
-int vn_blocks_per_sm() {
-    int nb = 0, nb2 = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_vn_update, 256, 0) != cudaSuccess) nb = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, k_vn_tile64, 256, 0) != cudaSuccess) nb2 = 1;
-    nb = std::min(nb, nb2);
+int finish_blocks_per_sm() {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_finish, 256, 0) != cudaSuccess) nb = 1;
     return nb > 0 ? nb : 1;
 }
 
@@ -786,9 +750,8 @@ void launch_cn(const CodeDev& cd, const Group& g, int rule, int D, int nd, int b
     }
 }
 
-void launch_vn(const CodeDev& cd, const Group& g, int grid, cudaStream_t s) {
-    if (g.B == 64) k_vn_tile64<<<grid, 256, 0, s>>>(cd, g);
-    else k_vn_update<<<grid, 256, 0, s>>>(cd, g);
+void launch_finish(const CodeDev& cd, const Group& g, int grid, cudaStream_t s) {
+    k_finish<<<grid, 256, 0, s>>>(cd, g);
 }
 
 void launch_check(const CodeDev& cd, const Group& g, int grid, int l, cudaStream_t s) {

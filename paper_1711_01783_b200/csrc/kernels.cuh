@@ -14,7 +14,8 @@ namespace metldpc {
 struct Group {
     int B, C;
     float* r;          // [E_it][B]   CN->VN messages r_ji of active edges (Eqs. 2-3)
-    float* L;          // [n_a][B]    posterior LLR of active VNs (Eq. 5)
+    float* L;          // [n_a][2][B] row of VN a: posterior LLR L (Eq. 5) at +0, the fixed-point
+                       //             accumulator of the next L (uint32, N3) at +B
     float* lam_a;      // [n_a][B]    channel LLR of active VNs (Eq. 1)
     float* lam1;       // [n_1][B]    channel LLR of degree-1 VNs, CSR slot order
     uint32_t* d1bits;  // [2][n_1][C] hard bits of degree-1 VNs, by iteration parity
@@ -49,14 +50,14 @@ int cn_tile_max(int D, int nd);          // CNs per warp tile the kernel stages
 int cn_units_per_tile(int D, int nd);    // warp units per tile (1: both chunks, 2: one each)
 extern const int kCnThreadsHost;
 size_t cn_smem(int rule, int D);
-int vn_blocks_per_sm();
+int finish_blocks_per_sm();
 
 void launch_scatter(const CodeDev& cd, const Group& g, const float* llr, int nb, cudaStream_t s);
 void launch_pack_syndrome(const CodeDev& cd, const Group& g, const uint32_t* synd, int nb, cudaStream_t s);
 void launch_init_ctl(const Group& g, int nb, cudaStream_t s);
 void launch_cn(const CodeDev& cd, const Group& g, int rule, int D, int nd, int begin, int count, int ts, int grid,
                int l, bool check, cudaStream_t s);
-void launch_vn(const CodeDev& cd, const Group& g, int grid, cudaStream_t s);
+void launch_finish(const CodeDev& cd, const Group& g, int grid, cudaStream_t s);
 void launch_check(const CodeDev& cd, const Group& g, int grid, int l, cudaStream_t s);
 void launch_latch(const Group& g, int l, bool final_, cudaStream_t s);
 void launch_finalize(const CodeDev& cd, const Group& g, int nb, uint32_t* bits_out, int32_t* iters_out,
