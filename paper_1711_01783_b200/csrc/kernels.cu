@@ -51,26 +51,50 @@ struct PhiT<METLDPC_RULE_PHI_LUT> {    // linear, 32 bins per binade
 // and the polynomial runs in ts = t / 2^J = bits(1.0 | low mantissa bits) - 1 (exact):
 // scaling by a power of two commutes with rounding, so every Horner intermediate is the
 // oracle's times 2^(J k) and the result is bit-identical to N2 as written.
+// (a & m) | c in one LOP3: c is kept in a register (an immediate would split the op in two).
+template <uint32_t M>
+__device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "n"(M), "r"(c));
+    return d;
+}
+
+// 1.0f as an opaque register value (see and_or).
+__device__ __forceinline__ uint32_t one_bits() {
+    uint32_t c;
+    asm("mov.b32 %0, 0x3F800000;" : "=r"(c));
+    return c;
+}
+
+// tabk: 32-bit shared-window address of this lane's table copy minus BIAS (phi_tab_lane).
 template <int RULE>
-__device__ __forceinline__ float phi_dev(const char* tabk, float y) {
+__device__ __forceinline__ float phi_dev(uint32_t tabk, float y, uint32_t one) {
     using P = PhiT<RULE>;
-    static_assert(P::STRIDE == (1 << (11 - P::J)), "(u >> (23 - J)) * STRIDE == (u & ~low) >> 12");
     constexpr uint32_t LOW = (1u << (23 - P::J)) - 1u;
     const uint32_t u = min(max(__float_as_uint(y), kPhiLoBits), kPhiHiBits);
-    const char* e = tabk + ((u & ~LOW) >> 12);
-    const float ts = __fsub_rn(__uint_as_float((u & LOW) | 0x3F800000u), 1.0f);
+    uint32_t e;   // tabk + bin * STRIDE as one IMAD (FMA pipe) after the shift
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(e) : "r"(u >> (23 - P::J)), "n"(P::STRIDE), "r"(tabk));
+    const float ts = __fsub_rn(__uint_as_float(and_or<LOW>(u, one)), 1.0f);
     if constexpr (RULE == METLDPC_RULE_EXACT) {
-        const float4 c = *reinterpret_cast<const float4*>(e);
+        float4 c;
+        asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(c.x), "=f"(c.y), "=f"(c.z), "=f"(c.w) : "r"(e));
         return __fmaf_rn(__fmaf_rn(__fmaf_rn(c.w, ts, c.z), ts, c.y), ts, c.x);
     } else {
-        const float2 c = *reinterpret_cast<const float2*>(e);
+        float2 c;
+        asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(c.x), "=f"(c.y) : "r"(e));
         return __fmaf_rn(c.y, ts, c.x);
     }
 }
 
+// The table copy of this lane as a 32-bit shared-window address with the bin bias folded
+// in, held opaquely in one register (the bin offset then costs SHF + LEA).
 template <int RULE>
-__device__ __forceinline__ const char* phi_tab_lane(const char* smem, int lane) {
-    return smem + (lane & 7) * PhiT<RULE>::ENTRY - PhiT<RULE>::BIAS;
+__device__ __forceinline__ uint32_t phi_tab_lane(const char* smem, int lane) {
+    const uint32_t a = uint32_t(__cvta_generic_to_shared(smem)) + uint32_t((lane & 7) * PhiT<RULE>::ENTRY) -
+                       uint32_t(PhiT<RULE>::BIAS);
+    uint32_t r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(a));
+    return r;
 }
 
 template <int RULE>
@@ -102,11 +126,12 @@ __device__ __forceinline__ uint32_t vn_fix(float o) {
 }
 
 template <int RULE, int NA, int ND>
-__device__ __forceinline__ uint32_t cn_lane(const char* tabk, const float (&Lv)[NA > 0 ? NA : 1],
+__device__ __forceinline__ uint32_t cn_lane(uint32_t tabk, const float (&Lv)[NA > 0 ? NA : 1],
                                             const float (&ro)[NA > 0 ? NA : 1], float lam, uint32_t sbit,
                                             uint32_t d1prev, float* pr, float* pla, const int (&offs)[NA > 0 ? NA : 1],
                                             const int* idx, bool act, uint32_t& d1bit) {
     constexpr int D = NA + ND;
+    const uint32_t one = one_bits();
     float p[D], P[D];
     uint32_t xb[D];     // bits of x + 0.0f: sign bit = [x < 0] exactly (-0 + 0 = +0), N1 / R2
     uint32_t par = sbit << 31;                            // bit 31: s_j XOR all n_k
@@ -117,12 +142,12 @@ __device__ __forceinline__ uint32_t cn_lane(const char* tabk, const float (&Lv)[
         chk ^= __float_as_uint(__fadd_rn(Lv[s], 0.0f)) >> 31;   // c_v^{l-1} = [L < 0] (-0 + 0 = +0)
         xb[s] = __float_as_uint(__fadd_rn(x, 0.0f));
         par ^= xb[s];
-        p[s] = phi_dev<RULE>(tabk, fabsf(x));
+        p[s] = phi_dev<RULE>(tabk, fabsf(x), one);
     }
     if constexpr (ND > 0) {                               // degree-1 VN sends its prior
         xb[NA] = __float_as_uint(__fadd_rn(lam, 0.0f));
         par ^= xb[NA];
-        p[NA] = phi_dev<RULE>(tabk, fabsf(lam));
+        p[NA] = phi_dev<RULE>(tabk, fabsf(lam), one);
     }
     // P_0 = 0, P_{k+1} = P_k + p_k; Q_{D-1} = 0, Q_k = Q_{k+1} + p_{k+1}; S_k = P_k + Q_k.
     // The additions with an exact +0 operand are skipped: p, P, Q >= +0, so 0 + v = v.
@@ -134,7 +159,7 @@ __device__ __forceinline__ uint32_t cn_lane(const char* tabk, const float (&Lv)[
 #pragma unroll
     for (int s = D - 1; s >= 0; --s) {
         const float S = (s == D - 1) ? P[s] : (s == 0 ? Q : __fadd_rn(P[s], Q));
-        const float mag = fminf(phi_dev<RULE>(tabk, S), kRMax);
+        const float mag = fminf(phi_dev<RULE>(tabk, S, one), kRMax);
         const float o = __uint_as_float(__float_as_uint(mag) | ((par ^ xb[s]) & 0x80000000u));
         if (s < NA) {
             if (act) {
@@ -185,7 +210,7 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
     if (threadIdx.x < 2) { s_unsat[threadIdx.x] = 0u; s_act[threadIdx.x] = g.act[threadIdx.x]; }
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const char* tabk = phi_tab_lane<RULE>(smem, lane);
+    const uint32_t tabk = phi_tab_lane<RULE>(smem, lane);
     int* s_idx = reinterpret_cast<int*>(smem + PT::TAB_BYTES) + warp * STAGE;
     const uint32_t am0 = s_act[0], am1 = s_act[1];
     const int wpb = blockDim.x >> 5;
@@ -311,7 +336,7 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group 
     if (threadIdx.x < g.C) { s_unsat[threadIdx.x] = 0u; s_act[threadIdx.x] = g.act[threadIdx.x]; }
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const char* tabk = phi_tab_lane<RULE>(smem, lane);
+    const uint32_t tabk = phi_tab_lane<RULE>(smem, lane);
     const int wpb = blockDim.x >> 5;
     const int lc = __ffs(g.C) - 1;
     const long total = long(count) << lc;
@@ -325,6 +350,7 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group 
         const int db = __ldg(cd.cn_dptr + j), d = na + (__ldg(cd.cn_dptr + j + 1) - db);
         const uint32_t sbit = (__ldg(g.synd_t + size_t(j) * g.C + c) >> lane) & 1u;
         const int idx = (lane < na) ? __ldg(cd.a_vn + ab + lane) : 0;
+        const uint32_t one = one_bits();
         float p[kMaxCnDeg], P[kMaxCnDeg], xs[kMaxCnDeg];
         uint32_t negmask = 0, chk = sbit;
         for (int s = 0; s < d; ++s) {
@@ -342,7 +368,7 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group 
             }
             xs[s] = x;
             negmask |= (__float_as_uint(__fadd_rn(x, 0.0f)) >> 31) << s;   // = [x < 0]
-            p[s] = phi_dev<RULE>(tabk, fabsf(x));
+            p[s] = phi_dev<RULE>(tabk, fabsf(x), one);
         }
         if (k.check) {
             const uint32_t mm = __ballot_sync(FULL, chk) & amask;
@@ -355,7 +381,7 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group 
         float Q = 0.0f;
         for (int s = d - 1; s >= 0; --s) {
             const float S = __fadd_rn(P[s], Q);
-            const float mag = fminf(phi_dev<RULE>(tabk, S), kRMax);
+            const float mag = fminf(phi_dev<RULE>(tabk, S, one), kRMax);
             const float o = __uint_as_float(__float_as_uint(mag) | ((par ^ ((negmask >> s) & 1u)) << 31));
             if (s < na) {
                 const int v = __shfl_sync(FULL, idx, s);      // whole warp: lane s may be an idle lane
