@@ -176,11 +176,141 @@ __device__ __forceinline__ uint32_t cn_lane(uint32_t tabk, const float (&Lv)[NA 
     return chk;
 }
 
+// ------------------------------------------------------------------ two-lane (fp32x2) helpers
+
+// sm_100a packed fp32 pairs: FADD2 / FFMA2 round each element to nearest like FADD / FFMA,
+// so a pair op is bit-identical to two scalar ops; it halves the instruction count of the
+// two codeword lanes a thread carries.
+__device__ __forceinline__ unsigned long long f2pack(float2 a) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+    return r;
+}
+__device__ __forceinline__ float2 f2unpack(unsigned long long r) {
+    float2 a;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+    return a;
+}
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2pack(a)), "l"(f2pack(b)));
+    return f2unpack(r);
+}
+__device__ __forceinline__ float2 f2sub(float2 a, float2 b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2pack(a)), "l"(f2pack(b)));
+    return f2unpack(r);
+}
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2pack(a)), "l"(f2pack(b)), "l"(f2pack(c)));
+    return f2unpack(r);
+}
+
+// phi of two lanes: integer bin/mantissa work per lane, ts - 1 as one FADD2.
+template <int RULE>
+__device__ __forceinline__ float2 phi_pair(uint32_t tabk, float y0, float y1, uint32_t one) {
+    using P = PhiT<RULE>;
+    constexpr uint32_t LOW = (1u << (23 - P::J)) - 1u;
+    const uint32_t u0 = min(max(__float_as_uint(y0), kPhiLoBits), kPhiHiBits);
+    const uint32_t u1 = min(max(__float_as_uint(y1), kPhiLoBits), kPhiHiBits);
+    uint32_t e0, e1;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(e0) : "r"(u0 >> (23 - P::J)), "n"(P::STRIDE), "r"(tabk));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(e1) : "r"(u1 >> (23 - P::J)), "n"(P::STRIDE), "r"(tabk));
+    const float2 ts = f2add(make_float2(__uint_as_float(and_or<LOW>(u0, one)), __uint_as_float(and_or<LOW>(u1, one))),
+                            make_float2(-1.0f, -1.0f));
+    float2 r;
+    if constexpr (RULE == METLDPC_RULE_EXACT) {
+        float4 c0, c1;
+        asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(c0.x), "=f"(c0.y), "=f"(c0.z), "=f"(c0.w) : "r"(e0));
+        asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(c1.x), "=f"(c1.y), "=f"(c1.z), "=f"(c1.w) : "r"(e1));
+        r.x = __fmaf_rn(__fmaf_rn(__fmaf_rn(c0.w, ts.x, c0.z), ts.x, c0.y), ts.x, c0.x);
+        r.y = __fmaf_rn(__fmaf_rn(__fmaf_rn(c1.w, ts.y, c1.z), ts.y, c1.y), ts.y, c1.x);
+    } else {
+        float2 c0, c1;
+        asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(c0.x), "=f"(c0.y) : "r"(e0));
+        asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(c1.x), "=f"(c1.y) : "r"(e1));
+        r.x = __fmaf_rn(c0.y, ts.x, c0.x);
+        r.y = __fmaf_rn(c1.y, ts.y, c1.x);
+    }
+    return r;
+}
+
+// DESIGN.md N1 for one CN and the two lanes (l, l + 32) of a thread, element-wise
+// identical to cn_lane (same fp32 operations, pairs where the two lanes do the same op).
+template <int RULE, int NA, int ND>
+__device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 0 ? NA : 1],
+                                         const float2 (&ro)[NA > 0 ? NA : 1], float2 lam, uint2 sbit, uint2 d1prev,
+                                         float* pr, float* pla, const int (&offs)[NA > 0 ? NA : 1], bool act0,
+                                         bool act1, uint2& d1bit) {
+    constexpr int D = NA + ND;
+    const uint32_t one = one_bits();
+    const float2 zero2 = make_float2(0.0f, 0.0f);
+    float2 p[D], P[D];
+    uint32_t xb0[D], xb1[D];
+    uint32_t par0 = sbit.x << 31, par1 = sbit.y << 31;
+    uint32_t chk0 = sbit.x ^ d1prev.x, chk1 = sbit.y ^ d1prev.y;
+#pragma unroll
+    for (int s = 0; s < NA; ++s) {
+        const float2 x = f2sub(Lv[s], ro[s]);                             // extrinsic q = L - r (R10)
+        const float2 Lz = f2add(Lv[s], zero2);                            // [L < 0] via sign of L + 0
+        chk0 ^= __float_as_uint(Lz.x) >> 31;
+        chk1 ^= __float_as_uint(Lz.y) >> 31;
+        const float2 xz = f2add(x, zero2);
+        xb0[s] = __float_as_uint(xz.x);
+        xb1[s] = __float_as_uint(xz.y);
+        par0 ^= xb0[s];
+        par1 ^= xb1[s];
+        p[s] = phi_pair<RULE>(tabk, fabsf(x.x), fabsf(x.y), one);
+    }
+    if constexpr (ND > 0) {
+        const float2 lz = f2add(lam, zero2);
+        xb0[NA] = __float_as_uint(lz.x);
+        xb1[NA] = __float_as_uint(lz.y);
+        par0 ^= xb0[NA];
+        par1 ^= xb1[NA];
+        p[NA] = phi_pair<RULE>(tabk, fabsf(lam.x), fabsf(lam.y), one);
+    }
+    P[0] = zero2;
+    if constexpr (D > 1) P[1] = p[0];
+#pragma unroll
+    for (int s = 2; s < D; ++s) P[s] = f2add(P[s - 1], p[s - 1]);
+    float2 Q = zero2;
+#pragma unroll
+    for (int s = D - 1; s >= 0; --s) {
+        const float2 S = (s == D - 1) ? P[s] : (s == 0 ? Q : f2add(P[s], Q));
+        const float2 ph = phi_pair<RULE>(tabk, S.x, S.y, one);
+        const float2 o = make_float2(
+            __uint_as_float(__float_as_uint(fminf(ph.x, kRMax)) | ((par0 ^ xb0[s]) & 0x80000000u)),
+            __uint_as_float(__float_as_uint(fminf(ph.y, kRMax)) | ((par1 ^ xb1[s]) & 0x80000000u)));
+        if (s < NA) {
+            const float2 fx = f2fma(o, make_float2(131072.0f, 131072.0f), make_float2(12582912.0f, 12582912.0f));
+            unsigned int* pa = reinterpret_cast<unsigned int*>(pla + offs[s] + 64);
+            if (act0) {
+                __stcs(pr + s * 64, o.x);
+                atomicAdd(pa, __float_as_uint(fx.x));          // VN sum (Eq. 4, N3)
+            }
+            if (act1) {
+                __stcs(pr + s * 64 + 32, o.y);
+                atomicAdd(pa + 32, __float_as_uint(fx.y));
+            }
+        } else {
+            const float2 dd = f2add(lam, o);
+            d1bit = make_uint2(uint32_t(dd.x < 0.0f), uint32_t(dd.y < 0.0f));   // Step 5 for VN_b
+        }
+        if (s > 0) Q = f2add(Q, p[s]);
+    }
+    return make_uint2(chk0, chk1);
+}
+
 // Asynchronous L2 prefetch of a contiguous range by the TMA unit (no registers held).
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+#ifndef METLDPC_CN_PAIR
+#define METLDPC_CN_PAIR 1   // two-lane path with packed fp32x2 ops (FADD2 / FFMA2)
+#endif
 #ifndef METLDPC_CN_PF
 #define METLDPC_CN_PF 0     // CNs of look-ahead for an r / lambda L2 prefetch (0: off; measured
 #endif                      // slower at 4 and 8 -- the kernel is issue-bound, not DRAM-latency-bound)
@@ -283,6 +413,23 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
                     for (int h = 0; h < LPT; ++h) lam[h] = 0.0f;
                 }
                 uint32_t chk[LPT], b[LPT];
+                if constexpr (LPT == 2 && METLDPC_CN_PAIR) {
+                    float2 L2[NAS], r2[NAS];
+#pragma unroll
+                    for (int s = 0; s < NA; ++s) {
+                        L2[s] = make_float2(Lv[0][s], Lv[1][s]);
+                        r2[s] = make_float2(ro[0][s], ro[1][s]);
+                    }
+                    uint2 d1 = make_uint2(0, 0);
+                    const uint2 c2 = cn_pair<RULE, NA, ND>(
+                        tabk, L2, r2, make_float2(lam[0], lam[1]), make_uint2((swx >> lane) & 1u, (swy >> lane) & 1u),
+                        make_uint2((wv.x >> lane) & 1u, (wv.y >> lane) & 1u), pr, pL, offs, ((am0 >> lane) & 1u) != 0u,
+                        ((am1 >> lane) & 1u) != 0u, d1);
+                    chk[0] = c2.x;
+                    chk[1] = c2.y;
+                    b[0] = d1.x;
+                    b[1] = d1.y;
+                } else {
 #pragma unroll
                 for (int h = 0; h < LPT; ++h) {
                     const int c = c0 + h;
@@ -292,6 +439,7 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
                     b[h] = 0;
                     chk[h] = cn_lane<RULE, NA, ND>(tabk, Lv[h], ro[h], lam[h], sbit, w[h], pr + h * 32, pL + h * 32, offs,
                                                    idx, act, b[h]);
+                }
                 }
 #pragma unroll
                 for (int h = 0; h < LPT; ++h) {
