@@ -54,6 +54,7 @@ struct metldpc_decoder_s {
     };
     int K = 1;
     std::vector<Workspace> ws;
+    std::vector<L2Window> l2w;                      // per workspace: persisting window over L rows
     std::vector<cudaStream_t> gs;                   // one stream per workspace (K > 1)
     std::vector<cudaEvent_t> fork_ev, join_ev;
     int last_ws = 0;                                // workspace of the last group decoded
@@ -234,7 +235,8 @@ void group_iter(metldpc_decoder d, const GroupJob& j, int l) {
     const bool et = d->cfg.early_term != 0;
     size_t e = ev_begin(d, 0, j.s);
     for (const auto& c : d->cn_classes) {
-        launch_cn(cd, g, d->cfg.rule, c.D, c.nd, c.begin, c.count, c.ts, c.grid, l, et && l >= 2, j.s);
+        launch_cn(cd, g, d->cfg.rule, c.D, c.nd, c.begin, c.count, c.ts, c.grid, l, et && l >= 2, j.s,
+                  d->l2w[size_t(j.k)]);
         d->prof.launches++;
     }
     ev_end(d, e, j.s);
@@ -245,7 +247,7 @@ void group_iter(metldpc_decoder d, const GroupJob& j, int l) {
         d->prof.launches++;
     }
     e = ev_begin(d, 1, j.s);
-    launch_finish(cd, g, d->vn_grid, j.s);
+    launch_finish(cd, g, d->vn_grid, j.s, d->l2w[size_t(j.k)]);
     ev_end(d, e, j.s);
     d->prof.vn_launches++;
     d->prof.launches++;
@@ -413,6 +415,30 @@ metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, cons
         }
         cudaMemset(w.d1bits, 0, 2 * size_t(L.n_1) * C * sizeof(uint32_t));
         cudaMemset(w.ctl, 0, 16 * sizeof(uint32_t));
+    }
+    // Persisting-L2 window over the workspace's L / accumulator rows (the CN gathers and
+    // atomics hit them ~23 times per iteration per VN).  Measured (round 1, C3): +2 % with one
+    // group in flight, strongly negative with 4 (the windows thrash the set-aside), so it is
+    // opt-in (METLDPC_L2PERSIST=1) and only applied when groups_in_flight == 1.
+    d->l2w.assign(size_t(d->K), L2Window{});
+    {
+        const char* e = std::getenv("METLDPC_L2PERSIST");
+        int max_persist = 0, max_window = 0;
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, code->device);
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, code->device);
+        const size_t rows = 2 * size_t(L.n_a) * B * sizeof(float);
+        if (e && *e == '1' && d->K == 1 && max_persist > 0 && max_window > 0) {
+            const size_t want = std::min(size_t(max_persist), rows * size_t(d->K));
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+            for (int k = 0; k < d->K; ++k) {
+                L2Window& w = d->l2w[size_t(k)];
+                w.base = d->ws[size_t(k)].L;
+                w.bytes = std::min(rows, size_t(max_window));
+                // share the persisting set-aside between the groups in flight
+                w.hit_ratio = float(std::min(1.0, double(want) / double(d->K) / double(w.bytes)));
+            }
+        }
+        cudaGetLastError();
     }
     if (d->K > 1) {
         d->gs.resize(size_t(d->K));

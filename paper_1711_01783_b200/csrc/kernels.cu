@@ -911,21 +911,45 @@ void launch_pack_syndrome(const CodeDev& cd, const Group& g, const uint32_t* syn
 
 void launch_init_ctl(const Group& g, int nb, cudaStream_t s) { k_init_ctl<<<1, 128, 0, s>>>(g, nb); }
 
+// Optional persisting-L2 window over the group's L / accumulator rows (set by the decoder
+// when the device supports it).
+static cudaError_t launch_with_window(void* f, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t s,
+                                      const L2Window& w) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    if (w.bytes) {
+        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[0].val.accessPolicyWindow.base_ptr = w.base;
+        attr[0].val.accessPolicyWindow.num_bytes = w.bytes;
+        attr[0].val.accessPolicyWindow.hitRatio = w.hit_ratio;
+        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    return cudaLaunchKernelExC(&cfg, f, args);
+}
+
 void launch_cn(const CodeDev& cd, const Group& g, int rule, int D, int nd, int begin, int count, int ts, int grid,
-               int l, bool check, cudaStream_t s) {
+               int l, bool check, cudaStream_t s, const L2Window& w) {
     CnCtl k{check ? 1 : 0, l == 1 ? 1 : 0, (l - 1) & 1, l & 1};
     void* f = cn_kernel(rule, D, nd);
     if (D < 0) {
         void* args[] = {const_cast<CodeDev*>(&cd), const_cast<Group*>(&g), &k, &begin, &count};
-        cudaLaunchKernel(f, dim3(grid), dim3(kCnThreads), args, cn_smem(rule, D, nd), s);
+        launch_with_window(f, dim3(grid), dim3(kCnThreads), args, cn_smem(rule, D, nd), s, w);
     } else {
         void* args[] = {const_cast<CodeDev*>(&cd), const_cast<Group*>(&g), &k, &begin, &count, &ts};
-        cudaLaunchKernel(f, dim3(grid), dim3(kCnThreads), args, cn_smem(rule, D, nd), s);
+        launch_with_window(f, dim3(grid), dim3(kCnThreads), args, cn_smem(rule, D, nd), s, w);
     }
 }
 
-void launch_finish(const CodeDev& cd, const Group& g, int grid, cudaStream_t s) {
-    k_finish<<<grid, 256, 0, s>>>(cd, g);
+void launch_finish(const CodeDev& cd, const Group& g, int grid, cudaStream_t s, const L2Window& w) {
+    void* args[] = {const_cast<CodeDev*>(&cd), const_cast<Group*>(&g)};
+    launch_with_window(reinterpret_cast<void*>(&k_finish), dim3(grid), dim3(256), args, 0, s, w);
 }
 
 void launch_check(const CodeDev& cd, const Group& g, int grid, int l, cudaStream_t s) {

@@ -43,6 +43,12 @@ struct CodeDev {
 };
 
 // returns the number of CTAs per SM the CN kernel reaches (for persistent grids)
+struct L2Window {          // persisting-L2 access window (bytes == 0: none)
+    void* base = nullptr;
+    size_t bytes = 0;
+    float hit_ratio = 1.0f;
+};
+
 // CN class kernels: total degree D in 0..16 with nd <= 1 degree-1 slots (tiled, unrolled)
 // or D = -1 (generic: more degree-1 slots or degree 17..32)
 int cn_blocks_per_sm(int rule, int D, int nd);
@@ -56,8 +62,8 @@ void launch_scatter(const CodeDev& cd, const Group& g, const float* llr, int nb,
 void launch_pack_syndrome(const CodeDev& cd, const Group& g, const uint32_t* synd, int nb, cudaStream_t s);
 void launch_init_ctl(const Group& g, int nb, cudaStream_t s);
 void launch_cn(const CodeDev& cd, const Group& g, int rule, int D, int nd, int begin, int count, int ts, int grid,
-               int l, bool check, cudaStream_t s);
-void launch_finish(const CodeDev& cd, const Group& g, int grid, cudaStream_t s);
+               int l, bool check, cudaStream_t s, const L2Window& w);
+void launch_finish(const CodeDev& cd, const Group& g, int grid, cudaStream_t s, const L2Window& w);
 void launch_check(const CodeDev& cd, const Group& g, int grid, int l, cudaStream_t s);
 void launch_latch(const Group& g, int l, bool final_, cudaStream_t s);
 void launch_finalize(const CodeDev& cd, const Group& g, int nb, uint32_t* bits_out, int32_t* iters_out,
