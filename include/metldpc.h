@@ -146,6 +146,24 @@ metldpc_status metldpc_llr_from_md(metldpc_decoder dec, int32_t batch, int32_t d
                                    const float* v, const float* xnorm, float* llr_out,
                                    uintptr_t cuda_stream);
 
+/* Alice's LLRs straight from her raw Gaussian block and Bob's rotation (the
+ * GPU MD front end): with M(alpha) w = alpha * w the d-dimensional
+ * division-algebra product (Cayley-Dickson: (a1,a2)(b1,b2) = (a1 b1 - conj(b2) a2,
+ * b2 a1 + a2 conj(b1))), lambda = c |x| M(alpha) x/|x| = c M(alpha) x, c = 2 sqrt(snr(1+snr))
+ * (R13).  fp32 per DESIGN.md N6: (alpha x)_i = fmaf left fold over the d terms, then * c.
+ *   x       dev fp32 [batch][n]  Alice's raw block values X
+ *   alpha   dev fp32 [batch][n]  Bob's rotation coefficients, d per block (as sent)
+ *   llr_out dev fp32 [batch][n]  may alias x. */
+metldpc_status metldpc_md_alice_llr(metldpc_decoder dec, int32_t batch, int32_t d, float snr,
+                                    const float* x, const float* alpha, float* llr_out,
+                                    uintptr_t cuda_stream);
+
+/* S = H c^T (Step 1: Bob's syndrome S_B of his string U; equally the S_A test of a
+ * decided word).  bits dev u32 [batch][ceil(n/32)], synd_out dev u32 [batch][ceil(m/32)],
+ * both LSB-first in the caller's VN / CN order. */
+metldpc_status metldpc_syndrome(metldpc_decoder dec, int32_t batch, const uint32_t* bits,
+                                uint32_t* synd_out, uintptr_t cuda_stream);
+
 /* ---------------------------------------------------------------- 3. decode */
 
 /* Syndrome BP decoding of a batch (P:117-146 Steps 2-5, flooding schedule, degree-1

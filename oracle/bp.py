@@ -60,6 +60,10 @@ def lib():
         _lib.orc_llr_from_md_f32.argtypes = [C.c_int, C.c_int, C.c_float, P, P, P]
         _lib.orc_llr_from_md_f64.restype = None
         _lib.orc_llr_from_md_f64.argtypes = [C.c_int, C.c_int, C.c_double, P, P, P]
+        _lib.orc_md_alice_f32.restype = None
+        _lib.orc_md_alice_f32.argtypes = [C.c_int, C.c_int, C.c_float, P, P, P]
+        _lib.orc_md_table.restype = None
+        _lib.orc_md_table.argtypes = [C.c_int, P, P]
         _lib.orc_init()
     return _lib
 
@@ -184,3 +188,19 @@ def step64(code, llr, synd_words, r_in, L_in, rule: int = RULE_EXACT):
     if rc:
         raise ValueError(f"malformed code (rc={rc})")
     return ro, Lo
+
+
+def md_alice_f32(x: np.ndarray, alpha: np.ndarray, snr: float, d: int = 8) -> np.ndarray:
+    """DESIGN.md N6: lambda = c * (alpha x) per d-block (octonion product in a fixed fmaf order)."""
+    x = np.ascontiguousarray(x, np.float32)
+    a = np.ascontiguousarray(alpha, np.float32)
+    out = np.empty_like(x)
+    lib().orc_md_alice_f32(x.size, d, float(snr), _p(x), _p(a), _p(out))
+    return out
+
+
+def md_table(d: int):
+    k = np.zeros(d * d, np.int32)
+    s = np.zeros(d * d, np.int32)
+    lib().orc_md_table(d, _p(k), _p(s))
+    return k.reshape(d, d), s.reshape(d, d)

@@ -485,3 +485,64 @@ void orc_llr_from_md_f64(int n, int d, double snr, const double* v, const double
     double c = 2.0 * sqrt(snr * (1.0 + snr));
     for (int i = 0; i < n; ++i) out[i] = c * (xnorm ? xnorm[i / d] : sqrt((double)d)) * v[i];
 }
+
+/* ------------------------------------------------------------------ MD on the raw block (NEXT #1) */
+
+/* Basis products of the d-dimensional Cayley-Dickson algebra (d = 1, 2, 4, 8) with
+ * (a1, a2)(b1, b2) = (a1 b1 - conj(b2) a2, b2 a1 + a2 conj(b1)): e_p e_q = sgn * e_r.
+ * Built recursively on basis indices (oracle's own implementation). */
+static void cd_basis(int d, int p, int q, int* r, int* sgn) {
+    if (d == 1) { *r = 0; *sgn = 1; return; }
+    int h = d / 2;
+    int pa = p >= h, qa = q >= h, pl = p % h, ql = q % h;
+    int rr, ss;
+    if (!pa && !qa) {            /* (a1,0)(b1,0) = (a1 b1, 0) */
+        cd_basis(h, pl, ql, &rr, &ss); *r = rr; *sgn = ss;
+    } else if (!pa && qa) {      /* (a1,0)(0,b2) = (0, b2 a1) */
+        cd_basis(h, ql, pl, &rr, &ss); *r = h + rr; *sgn = ss;
+    } else if (pa && !qa) {      /* (0,a2)(b1,0) = (0, a2 conj(b1)) */
+        cd_basis(h, pl, ql, &rr, &ss); *r = h + rr; *sgn = ss * ((ql == 0) ? 1 : -1);
+    } else {                     /* (0,a2)(0,b2) = (-conj(b2) a2, 0) */
+        cd_basis(h, ql, pl, &rr, &ss); *r = rr; *sgn = -ss * ((ql == 0) ? 1 : -1);
+    }
+}
+
+/* DESIGN.md N6: (a b)_i = sum over q of sgn * a_p * b_q with e_p e_q = sgn e_i, evaluated
+ * as acc = fmaf(sgn * a_p, b_q, acc) for q = 0..d-1 from acc = 0; lambda_i = c * (alpha x)_i
+ * with c = (float)(2 sqrt(snr (1 + snr))) -- since M(alpha) is linear, c |x| (alpha x^)_i =
+ * c (alpha x)_i (R13 without the normalisation). */
+void orc_md_alice_f32(int n, int d, float snr, const float* x, const float* alpha, float* out) {
+    int kp[8][8], ks[8][8];
+    for (int i = 0; i < d; ++i)
+        for (int q = 0; q < d; ++q)
+            for (int p = 0; p < d; ++p) {
+                int r, sg;
+                cd_basis(d, p, q, &r, &sg);
+                if (r == i) { kp[i][q] = p; ks[i][q] = sg; }
+            }
+    double s = (double)snr;
+    float c = (float)(2.0 * sqrt(s * (1.0 + s)));
+    for (int b = 0; b < n / d; ++b) {
+        const float* a = alpha + (size_t)b * d;
+        const float* xb = x + (size_t)b * d;
+        for (int i = 0; i < d; ++i) {
+            float acc = 0.0f;
+            for (int q = 0; q < d; ++q) {
+                float ap = ks[i][q] > 0 ? a[kp[i][q]] : -a[kp[i][q]];
+                acc = fmaf(ap, xb[q], acc);
+            }
+            out[(size_t)b * d + i] = c * acc;
+        }
+    }
+}
+
+/* Basis table for tests: k[i*d + q] = p, s[i*d + q] = sgn. */
+void orc_md_table(int d, int* k, int* sg) {
+    for (int i = 0; i < d; ++i)
+        for (int q = 0; q < d; ++q)
+            for (int p = 0; p < d; ++p) {
+                int r, s2;
+                cd_basis(d, p, q, &r, &s2);
+                if (r == i) { k[i * d + q] = p; sg[i * d + q] = s2; }
+            }
+}

@@ -67,6 +67,9 @@ SYMBOLS = {
     "metldpc_decoder_destroy": (None, [C.c_void_p]),
     "metldpc_llr_from_md": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_float, C.c_void_p, C.c_void_p,
                                       C.c_void_p, C.c_size_t]),
+    "metldpc_md_alice_llr": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_float, C.c_void_p, C.c_void_p,
+                                       C.c_void_p, C.c_size_t]),
+    "metldpc_syndrome": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_size_t]),
     "metldpc_decode": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p,
                                  C.c_void_p, C.c_void_p, C.c_size_t]),
     "metldpc_decode_host": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p,
@@ -174,6 +177,15 @@ def metldpc_llr_from_md(dec, batch, d, snr, v, xnorm, llr_out, stream=None):
                                      _stream(stream)), "metldpc_llr_from_md")
 
 
+def metldpc_md_alice_llr(dec, batch, d, snr, x, alpha, llr_out, stream=None):
+    _check(lib().metldpc_md_alice_llr(dec, batch, d, float(snr), _ptr(x), _ptr(alpha), _ptr(llr_out),
+                                      _stream(stream)), "metldpc_md_alice_llr")
+
+
+def metldpc_syndrome(dec, batch, bits, synd_out, stream=None):
+    _check(lib().metldpc_syndrome(dec, batch, _ptr(bits), _ptr(synd_out), _stream(stream)), "metldpc_syndrome")
+
+
 def metldpc_decode(dec, batch, llr, syndrome, max_iter, bits_out, iters_out, converged_out, stream=None):
     _check(lib().metldpc_decode(dec, batch, _ptr(llr), _ptr(syndrome), max_iter, _ptr(bits_out), _ptr(iters_out),
                                 _ptr(converged_out), _stream(stream)), "metldpc_decode")
@@ -272,6 +284,20 @@ class Decoder:
         if out is None:
             out = torch.empty_like(v)
         metldpc_llr_from_md(self.h, batch, d, snr, v, xnorm, out, stream)
+        return out
+
+    def md_alice_llr(self, x, alpha, snr: float, d: int = 8, out=None, stream=None):
+        import torch
+        if out is None:
+            out = torch.empty_like(x)
+        metldpc_md_alice_llr(self.h, x.shape[0], d, snr, x, alpha, out, stream)
+        return out
+
+    def syndrome(self, bits, out=None, stream=None):
+        import torch
+        if out is None:
+            out = torch.empty((bits.shape[0], (self.code.m + 31) // 32), dtype=torch.int32, device=bits.device)
+        metldpc_syndrome(self.h, bits.shape[0], bits, out, stream)
         return out
 
     def decode(self, llr, syndrome, max_iter: int = 0, stream=None, out=None):

@@ -322,7 +322,8 @@ metldpc_status metldpc_code_create(int32_t device, int32_t n, int32_t m, int64_t
     if ((s = upload(&c->d_cn_aptr, L.cn_aptr)) || (s = upload(&c->d_cn_dptr, L.cn_dptr)) ||
         (s = upload(&c->d_a_vn, L.a_vn)) || (s = upload(&c->d_vn_aptr, L.vn_aptr)) ||
         (s = upload(&c->d_vn_aedge, L.vn_aedge)) || (s = upload(&c->d_vmap, L.vmap)) ||
-        (s = upload(&c->d_cn_new, L.cn_new)) ||
+        (s = upload(&c->d_cn_new, L.cn_new)) || (s = upload(&c->d_csr_ptr, L.csr_ptr)) ||
+        (s = upload(&c->d_csr_vn, L.csr_vn)) ||
         (s = upload(&c->d_phi_exact, te)) || (s = upload(&c->d_phi_lut, tl))) {
         metldpc_code_destroy(c);
         return s;
@@ -358,6 +359,8 @@ void metldpc_code_destroy(metldpc_code c) {
     dfree(c->d_vn_aedge);
     dfree(c->d_vmap);
     dfree(c->d_cn_new);
+    dfree(c->d_csr_ptr);
+    dfree(c->d_csr_vn);
     dfree(c->d_phi_exact);
     dfree(c->d_phi_lut);
     delete c;
@@ -521,6 +524,44 @@ metldpc_status metldpc_llr_from_md(metldpc_decoder d, int32_t batch, int32_t dim
     const double sd = double(snr);
     const float c = float(2.0 * std::sqrt(sd * (1.0 + sd)));
     launch_md_llr(int64_t(batch) * n, n, dim, c, v, xnorm, llr_out, reinterpret_cast<cudaStream_t>(stream));
+    d->prof.launches++;
+    CUDA_TRY(cudaGetLastError());
+    return METLDPC_OK;
+}
+
+// ------------------------------------------------------------------ MD front end, syndrome
+
+metldpc_status metldpc_md_alice_llr(metldpc_decoder d, int32_t batch, int32_t dim, float snr, const float* x,
+                                    const float* alpha, float* llr_out, uintptr_t stream) {
+    if (!d) return fail(METLDPC_EINVAL, "NULL decoder");
+    const int n = d->code->host.n;
+    if (batch < 0 || batch > d->max_batch) return fail(METLDPC_EINVAL, "batch out of range");
+    if (dim != 1 && dim != 2 && dim != 4 && dim != 8) return fail(METLDPC_EINVAL, "d must be 1, 2, 4 or 8");
+    if (n % dim) return fail(METLDPC_EINVAL, "n must be divisible by d");
+    if (!(snr > 0.0f) || !std::isfinite(snr)) return fail(METLDPC_EINVAL, "snr must be finite and > 0");
+    if (batch == 0) return METLDPC_OK;
+    if (!x || !alpha || !llr_out) return fail(METLDPC_EINVAL, "NULL buffer");
+    cudaSetDevice(d->code->device);
+    MdTable t{};
+    md_product_table(dim, t.kp, t.ks);
+    const double sd = double(snr);
+    const float c = float(2.0 * std::sqrt(sd * (1.0 + sd)));
+    launch_md_alice(int64_t(batch) * (n / dim), dim, c, x, alpha, llr_out, t, reinterpret_cast<cudaStream_t>(stream));
+    d->prof.launches++;
+    CUDA_TRY(cudaGetLastError());
+    return METLDPC_OK;
+}
+
+metldpc_status metldpc_syndrome(metldpc_decoder d, int32_t batch, const uint32_t* bits, uint32_t* synd_out,
+                                uintptr_t stream) {
+    if (!d) return fail(METLDPC_EINVAL, "NULL decoder");
+    if (batch < 0) return fail(METLDPC_EINVAL, "batch < 0");
+    if (batch == 0) return METLDPC_OK;
+    if (!bits || !synd_out) return fail(METLDPC_EINVAL, "NULL buffer");
+    cudaSetDevice(d->code->device);
+    const HostLayout& L = d->code->host;
+    launch_syndrome(d->code->d_csr_ptr, d->code->d_csr_vn, L.n, L.m, batch, bits, synd_out,
+                    reinterpret_cast<cudaStream_t>(stream));
     d->prof.launches++;
     CUDA_TRY(cudaGetLastError());
     return METLDPC_OK;

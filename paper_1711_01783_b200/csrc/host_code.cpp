@@ -155,6 +155,8 @@ metldpc_status build_layout(int32_t n, int32_t m, int64_t E, const int64_t* cn_p
         for (int64_t k = vn_ptr[v]; k < vn_ptr[v + 1]; ++k) L.vn_aedge.push_back(act_id[vn_edge[k]]);
     }
     L.vn_aptr[n_a] = int32_t(L.vn_aedge.size());
+    L.csr_ptr.assign(cn_ptr, cn_ptr + m + 1);
+    L.csr_vn.assign(edge_vn, edge_vn + E);
     return METLDPC_OK;
 }
 
@@ -224,6 +226,43 @@ std::vector<float> phi_device_table(int rule) {
             for (int q = 0; q < per; ++q)
                 dev[(size_t(b) * kPhiCopies + k) * per + q] = std::ldexp(base[size_t(b) * per + q], J * q);
     return dev;
+}
+
+// ------------------------------------------------------------------ MD product table (N6)
+
+// Cayley-Dickson product of two d-vectors, (a1, a2)(b1, b2) = (a1 b1 - conj(b2) a2,
+// b2 a1 + a2 conj(b1)), on doubles; basis products are read off e_p * e_q.
+static void cd_conj(const double* a, int d, double* out) {
+    out[0] = a[0];
+    for (int i = 1; i < d; ++i) out[i] = -a[i];
+}
+static void cd_mul_vec(const double* a, const double* b, int d, double* out) {
+    if (d == 1) { out[0] = a[0] * b[0]; return; }
+    const int h = d / 2;
+    double t1[8], t2[8], cb2[8], cb1[8];
+    cd_conj(b + h, h, cb2);
+    cd_conj(b, h, cb1);
+    cd_mul_vec(a, b, h, t1);
+    cd_mul_vec(cb2, a + h, h, t2);
+    for (int i = 0; i < h; ++i) out[i] = t1[i] - t2[i];
+    cd_mul_vec(b + h, a, h, t1);
+    cd_mul_vec(a + h, cb1, h, t2);
+    for (int i = 0; i < h; ++i) out[h + i] = t1[i] + t2[i];
+}
+
+void md_product_table(int d, int8_t* kp, int8_t* ks) {
+    for (int p = 0; p < d; ++p)
+        for (int q = 0; q < d; ++q) {
+            double ep[8] = {0}, eq[8] = {0}, r[8];
+            ep[p] = 1.0;
+            eq[q] = 1.0;
+            cd_mul_vec(ep, eq, d, r);
+            for (int i = 0; i < d; ++i)
+                if (r[i] != 0.0) {           // e_p e_q = sgn e_i
+                    kp[i * d + q] = int8_t(p);
+                    ks[i * d + q] = int8_t(r[i] > 0 ? 1 : -1);
+                }
+        }
 }
 
 // ------------------------------------------------------------------ alist

@@ -46,6 +46,8 @@ struct HostLayout {
     std::vector<int32_t> act_vn;    // [n_a] original VN id of active index
     std::vector<int32_t> cn_new;    // [m] original CN id -> j'
     std::vector<int32_t> perm_r;    // [E_it] t -> canonical active-edge id
+    std::vector<int32_t> csr_ptr;   // [m+1] caller's CSR row offsets (int32)
+    std::vector<int32_t> csr_vn;    // [E]   caller's CSR edge VNs
     // CN degree classes: contiguous j' ranges with one total degree D <= 16 and nd <= 1
     // degree-1 slots (a kernel instantiation per (D, nd), registers sized for it), or the
     // generic class (D = -1: nd >= 2 or degree 17..32).
@@ -68,6 +70,8 @@ void phi_table_lut(float* out /*kPhiBinsLut*2*/);
 // replicated device layout [bin 0..nbins (sentinel)][copy][coefficients]
 std::vector<float> phi_device_table(int rule);
 float phi_top();
+// Cayley-Dickson basis table for d in {1,2,4,8}: (a b)_i = sum_q ks[i d + q] a_{kp[i d + q]} b_q.
+void md_product_table(int d, int8_t* kp, int8_t* ks);
 
 }  // namespace metldpc
 
@@ -82,6 +86,8 @@ struct metldpc_code_s {
     int32_t* d_vn_aedge = nullptr;
     int32_t* d_vmap = nullptr;
     int32_t* d_cn_new = nullptr;
+    int32_t* d_csr_ptr = nullptr;   // original CSR (int32) for the syndrome kernel (Step 1)
+    int32_t* d_csr_vn = nullptr;
     float* d_phi_exact = nullptr;   // (kPhiBinsExact + 1) * 8 copies * 4
     float* d_phi_lut = nullptr;     // (kPhiBinsLut + 1) * 8 copies * 2
     int num_sms = 148;

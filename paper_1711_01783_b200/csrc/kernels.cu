@@ -817,6 +817,78 @@ __global__ void __launch_bounds__(256) k_md_llr(int64_t total, int n, int d, flo
     }
 }
 
+// ------------------------------------------------------------------ MD front end
+
+// Alice's LLRs from her raw block x and Bob's rotation alpha: M(alpha) is
+// linear, so c |x| (alpha x^)_i = c (alpha x)_i -- DESIGN.md N6: (alpha x)_i evaluated as
+// acc = fmaf(+-alpha_p, x_q, acc) for q = 0..D-1 from 0, lambda_i = c * acc.
+template <int D>
+__global__ void __launch_bounds__(256) k_md_alice(int64_t nblk, float c, const float* __restrict__ x,
+                                                  const float* __restrict__ alpha, float* __restrict__ out,
+                                                  MdTable t) {
+    for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < nblk; b += int64_t(gridDim.x) * blockDim.x) {
+        float a[D], xv[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            a[i] = __ldg(alpha + b * D + i);
+            xv[i] = __ldcs(x + b * D + i);
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            float acc = 0.0f;
+#pragma unroll
+            for (int q = 0; q < D; ++q) {
+                const float ap = (t.ks[i * D + q] > 0) ? a[t.kp[i * D + q]] : -a[t.kp[i * D + q]];
+                acc = __fmaf_rn(ap, xv[q], acc);
+            }
+            out[b * D + i] = __fmul_rn(c, acc);
+        }
+    }
+}
+
+// S = H c^T for frame-major bit-packed words (Step 1: Bob's syndrome of U; also a
+// checker of any decided word).  Warp = 32 consecutive CNs of one frame.
+__global__ void __launch_bounds__(256) k_syndrome(const int32_t* __restrict__ csr_ptr, const int32_t* __restrict__ csr_vn,
+                                                  int n, int m, int batch, const uint32_t* __restrict__ bits,
+                                                  uint32_t* __restrict__ synd) {
+    const int W = (m + 31) >> 5, NW = (n + 31) >> 5;
+    const int lane = threadIdx.x & 31;
+    const long items = long(W) * batch;
+    for (long it = (long(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; it < items;
+         it += (long(gridDim.x) * blockDim.x) >> 5) {
+        const int f = int(it / W), w = int(it - long(f) * W);
+        const int j = w * 32 + lane;
+        uint32_t par = 0;
+        if (j < m) {
+            const uint32_t* bf = bits + size_t(f) * NW;
+            for (int e = __ldg(csr_ptr + j); e < __ldg(csr_ptr + j + 1); ++e) {
+                const int v = __ldg(csr_vn + e);
+                par ^= (__ldg(bf + (v >> 5)) >> (v & 31)) & 1u;
+            }
+        }
+        const uint32_t word = __ballot_sync(FULL, par);
+        if (lane == 0) synd[size_t(f) * W + w] = word;
+    }
+}
+
+void launch_md_alice(int64_t nblk, int d, float c, const float* x, const float* alpha, float* out, const MdTable& t,
+                     cudaStream_t s) {
+    const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>((nblk + 255) / 256, 148 * 16)));
+    switch (d) {
+        case 1: k_md_alice<1><<<grid, 256, 0, s>>>(nblk, c, x, alpha, out, t); break;
+        case 2: k_md_alice<2><<<grid, 256, 0, s>>>(nblk, c, x, alpha, out, t); break;
+        case 4: k_md_alice<4><<<grid, 256, 0, s>>>(nblk, c, x, alpha, out, t); break;
+        default: k_md_alice<8><<<grid, 256, 0, s>>>(nblk, c, x, alpha, out, t); break;
+    }
+}
+
+void launch_syndrome(const int32_t* csr_ptr, const int32_t* csr_vn, int n, int m, int batch, const uint32_t* bits,
+                     uint32_t* synd, cudaStream_t s) {
+    const long warps = long((m + 31) / 32) * batch;
+    const unsigned grid = unsigned(std::max<long>(1, std::min<long>((warps + 7) / 8, 148 * 16)));
+    k_syndrome<<<grid, 256, 0, s>>>(csr_ptr, csr_vn, n, m, batch, bits, synd);
+}
+
 // ------------------------------------------------------------------ batch counters (a7)
 
 __global__ void k_counters(int batch, const int32_t* __restrict__ iters, const uint8_t* __restrict__ conv,

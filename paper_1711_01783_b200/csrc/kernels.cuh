@@ -68,6 +68,13 @@ void launch_check(const CodeDev& cd, const Group& g, int grid, int l, cudaStream
 void launch_latch(const Group& g, int l, bool final_, cudaStream_t s);
 void launch_finalize(const CodeDev& cd, const Group& g, int nb, uint32_t* bits_out, int32_t* iters_out,
                      uint8_t* conv_out, cudaStream_t s);
+struct MdTable {
+    int8_t kp[64], ks[64];
+};
+void launch_md_alice(int64_t blocks_total, int d, float c, const float* x, const float* alpha, float* out,
+                     const MdTable& t, cudaStream_t s);
+void launch_syndrome(const int32_t* csr_ptr, const int32_t* csr_vn, int n, int m, int batch, const uint32_t* bits,
+                     uint32_t* synd, cudaStream_t s);
 void launch_counters(int batch, const int32_t* iters, const uint8_t* conv, int64_t* out, cudaStream_t s);
 void launch_md_llr(int64_t total, int n, int d, float c, const float* v, const float* xnorm, float* out,
                    cudaStream_t s);

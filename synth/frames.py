@@ -102,10 +102,11 @@ def gen_frame(code: Code, snr: float, data_key: int, frame_id: int, d: int = 8) 
     alpha = md_bob(y, u, d)
     v, xn = md_alice(x, alpha, d)
     return {"u": u, "v": v.astype(np.float32), "xnorm": xn.astype(np.float32),
-            "synd": syndrome_words(code, u), "frame_id": frame_id}
+            "synd": syndrome_words(code, u), "frame_id": frame_id,
+            "x": x.astype(np.float32), "alpha": alpha.reshape(-1).astype(np.float32)}
 
 
 def gen_batch(code: Code, snr: float, data_key: int, frame_ids, d: int = 8) -> dict:
     fr = [gen_frame(code, snr, data_key, f, d) for f in frame_ids]
-    return {k: np.stack([f[k] for f in fr]) for k in ("u", "v", "xnorm", "synd")} | {
+    return {k: np.stack([f[k] for f in fr]) for k in ("u", "v", "xnorm", "synd", "x", "alpha")} | {
         "frame_ids": np.asarray(list(frame_ids))}

@@ -264,3 +264,61 @@ def test_c3_full_size_sampled_lane(rule):
         o = bp.decode(code, lam, fr["synd"][i], 100, rule=rule, prec=32)
         _assert_frame_equal(code, o, bits[i], iters[i], conv[i], f"lane {i}")
     assert (iters > 0).all()
+
+
+def test_c4_rate005_full_size_sampled_lane():
+    """C4 (configs[3]): rate-0.05 stand-in (Table-1 counts: E 3,480,000, m 950,000,
+    930,000 degree-1 VNs), n = 10^6, SNR 0.076, N = 150 (R15), 64-lane groups: one sampled
+    lane replayed by the oracle bit-exactly; classes (2,1), (3,1), (8,0), (9,0) all run
+    the specialised kernels."""
+    code = make_met_code("r0.05", 10 ** 6)
+    h = B.Code(code)
+    assert (h.info.edges, h.info.iter_edges, h.info.m) == (3480000, 2550000, 950000)
+    nf = 64
+    fr = gen_batch(code, 0.076, 0, range(nf))
+    dec = B.Decoder(h, nf, rule=B.RULE_EXACT, max_iter=150)
+    llr_d = dec.llr_from_md(torch.from_numpy(fr["v"]).cuda(), torch.from_numpy(fr["xnorm"]).cuda(), 0.076)
+    bits, iters, conv = dec.decode(llr_d, torch.from_numpy(fr["synd"].view(np.int32)).cuda())
+    bits = bits.cpu().numpy().view(np.uint32)
+    iters = iters.cpu().numpy()
+    conv = conv.cpu().numpy()
+    i = 41
+    lam = bp.llr_from_md_f32(fr["v"][i], fr["xnorm"][i], 0.076)
+    o = bp.decode(code, lam, fr["synd"][i], 150, rule=B.RULE_EXACT, prec=32)
+    _assert_frame_equal(code, o, bits[i], iters[i], conv[i], f"lane {i}")
+    assert (iters > 0).all()
+
+
+@pytest.mark.parametrize("d", [8, 4, 2, 1])
+def test_md_alice_llr_bit_exact(c1, d):
+    """GPU MD front end (metldpc_md_alice_llr, N6) bit-identical to the oracle."""
+    code, h = c1
+    from synth.frames import md_bob
+    rng = np.random.default_rng(30 + d)
+    nb = 5
+    x = rng.standard_normal((nb, code.n)).astype(np.float32)
+    u = rng.integers(0, 2, (nb, code.n)).astype(np.uint8)
+    y = x + rng.standard_normal((nb, code.n)).astype(np.float32) * 2.5
+    alpha = np.stack([md_bob(y[i].astype(np.float64), u[i], d).reshape(-1) for i in range(nb)]).astype(np.float32)
+    dec = B.Decoder(h, 8)
+    got = dec.md_alice_llr(torch.from_numpy(x).cuda(), torch.from_numpy(alpha).cuda(), 0.161, d=d).cpu().numpy()
+    for i in range(nb):
+        ref = bp.md_alice_f32(x[i], alpha[i], 0.161, d)
+        assert np.array_equal(got[i].view(np.uint32), ref.view(np.uint32)), i
+
+
+def test_syndrome_kernel(c1):
+    """metldpc_syndrome (Step 1) = Bob's S_B of U (synth) and = the oracle's H c of decoded words."""
+    code, h = c1
+    fr = _frames(code, [(0.3, 3), (0.161, 3)])
+    dec = B.Decoder(h, 8)
+    ub = np.stack([pack_bits(u) for u in fr["u"]])
+    s = dec.syndrome(torch.from_numpy(ub.view(np.int32)).cuda()).cpu().numpy().view(np.uint32)
+    assert np.array_equal(s, fr["synd"])
+    llr = _llr_oracle(fr)
+    _, bits, iters, conv = _gpu_decode(h, llr, fr["synd"], B.RULE_EXACT, 20)
+    s2 = dec.syndrome(torch.from_numpy(bits.view(np.int32)).cuda()).cpu().numpy().view(np.uint32)
+    for i in range(len(llr)):
+        ref = pack_bits(bp.syndrome(code, unpack_bits(bits[i], code.n)))
+        assert np.array_equal(s2[i], ref)
+        assert bool(conv[i]) == np.array_equal(s2[i], fr["synd"][i])

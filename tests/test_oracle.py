@@ -309,3 +309,37 @@ def test_llr_from_md_properties():
     # closed form at one point: snr = 1 -> c = 2 sqrt(2); xnorm NULL -> sqrt(8)
     one = bp.llr_from_md_f64(np.array([0.5] * 8), None, 1.0)
     assert one[0] == pytest.approx(2 * math.sqrt(2) * math.sqrt(8) * 0.5, rel=1e-15)
+
+
+# ----------------------------------------------------------------- MD front end (N6)
+
+@pytest.mark.parametrize("d", [1, 2, 4, 8])
+def test_md_product_table_and_alice_llr(d):
+    """The oracle's division-algebra table reproduces synth's independent Cayley-Dickson
+    product; lambda = c (alpha x) equals the normalised form c |x| (alpha x^) of R13 up to
+    fp32 rounding (M(alpha) is linear), and noiseless blocks give lambda = c |y| u~."""
+    from synth.frames import cd_mul, md_alice, md_bob
+    rng = np.random.default_rng(d)
+    a = rng.standard_normal((500, d))
+    b = rng.standard_normal((500, d))
+    k, s = bp.md_table(d)
+    got = np.zeros_like(a)
+    for i in range(d):
+        for q in range(d):
+            got[:, i] += s[i, q] * a[:, k[i, q]] * b[:, q]
+    assert np.abs(got - cd_mul(a, b)).max() < 1e-12
+    n = 64 * d
+    x = rng.standard_normal(n)
+    u = rng.integers(0, 2, n).astype(np.uint8)
+    y = x + rng.standard_normal(n) * 2.0
+    alpha = md_bob(y, u, d).reshape(-1)
+    snr = 0.161
+    lam = bp.md_alice_f32(x.astype(np.float32), alpha.astype(np.float32), snr, d).astype(np.float64)
+    v, xn = md_alice(x, alpha.reshape(-1, d), d)
+    ref = 2 * math.sqrt(snr * (1 + snr)) * np.repeat(xn, d) * v
+    assert np.allclose(lam, ref, rtol=1e-5, atol=1e-5)
+    # noiseless: x = y -> alpha x = |y| u~
+    alpha0 = md_bob(x, u, d).reshape(-1)
+    lam0 = bp.md_alice_f32(x.astype(np.float32), alpha0.astype(np.float32), snr, d).astype(np.float64)
+    xn0 = np.repeat(np.linalg.norm(x.reshape(-1, d), axis=1), d)
+    assert np.allclose(lam0, 2 * math.sqrt(snr * (1 + snr)) * xn0 * (1 - 2.0 * u) / math.sqrt(d), rtol=1e-5, atol=1e-5)
