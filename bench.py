@@ -170,7 +170,8 @@ def measured_peak_gbs() -> tuple[float, str]:
 
 
 def workload_name(a) -> str:
-    return (f"C3: MET-LDPC {a.family} stand-in n={a.n}, SNR {a.snr}, max {a.iters} iterations "
+    tag = {"r0.1": "C3", "r0.05": "C4"}.get(a.family, "custom") if a.n == 1_000_000 else "custom"
+    return (f"{tag}: MET-LDPC {a.family} stand-in n={a.n}, SNR {a.snr}, max {a.iters} iterations "
             f"{'fixed' if a.no_et else 'with per-frame syndrome early termination'}, "
             f"{a.frames} frames/GPU per step, 8-D MD LLR input")
 
