@@ -55,6 +55,10 @@ struct metldpc_decoder_s {
     int K = 1;
     std::vector<Workspace> ws;
     std::vector<L2Window> l2w;                      // per workspace: persisting window over L rows
+    // CUDA-graph iteration loop per workspace: a conditional WHILE node whose
+    // body is CN classes -> latch -> finish -> loop control; built on first use.
+    std::vector<cudaGraphExec_t> loop_exec;
+    int use_graph = 1;
     std::vector<cudaStream_t> gs;                   // one stream per workspace (K > 1)
     std::vector<cudaEvent_t> fork_ev, join_ev;
     int last_ws = 0;                                // workspace of the last group decoded
@@ -134,6 +138,8 @@ Group group_of(metldpc_decoder d, int k) {
     g.iters = w.iters;
     g.conv = w.conv;
     g.done = w.done;
+    g.iter = reinterpret_cast<int32_t*>(w.ctl + 12);
+    g.maxit = reinterpret_cast<int32_t*>(w.ctl + 13);
     return g;
 }
 
@@ -216,13 +222,13 @@ struct GroupJob {
     cudaEvent_t done = nullptr;    // optional: recorded on the group's stream after finalize
 };
 
-metldpc_status group_begin(metldpc_decoder d, const GroupJob& j) {
+metldpc_status group_begin(metldpc_decoder d, const GroupJob& j, int N) {
     const CodeDev cd = code_dev(d->code, d->cfg.rule);
     const Group g = group_of(d, j.k);
     CUDA_TRY(cudaMemsetAsync(d->ws[size_t(j.k)].ctl + 8, 0, 4 * sizeof(uint32_t), j.s));
     launch_scatter(cd, g, j.llr, j.nb, j.s);
     launch_pack_syndrome(cd, g, j.synd, j.nb, j.s);
-    launch_init_ctl(g, j.nb, j.s);
+    launch_init_ctl(g, j.nb, N, j.s);
     d->prof.launches += 3;
     return METLDPC_OK;
 }
@@ -265,6 +271,71 @@ metldpc_status group_end(metldpc_decoder d, const GroupJob& j, int N) {
     return METLDPC_OK;
 }
 
+// Builds (once per workspace) the graph  while (l <= N && lanes left) { CN classes; latch;
+// finish; l++ }  with the iteration number and N in device memory (Group::iter / maxit).
+metldpc_status loop_graph(metldpc_decoder d, int k, cudaGraphExec_t* out) {
+    if (d->loop_exec[size_t(k)]) {
+        *out = d->loop_exec[size_t(k)];
+        return METLDPC_OK;
+    }
+    const CodeDev cd = code_dev(d->code, d->cfg.rule);
+    const Group g = group_of(d, k);
+    const bool et = d->cfg.early_term != 0;
+    cudaGraph_t graph;
+    CUDA_TRY(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle h;
+    CUDA_TRY(cudaGraphConditionalHandleCreate(&h, graph, 1u, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CUDA_TRY(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    cudaStream_t cs;
+    CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    for (const auto& c : d->cn_classes)
+        launch_cn(cd, g, d->cfg.rule, c.D, c.nd, c.begin, c.count, c.ts, c.grid, 0, et, cs, d->l2w[size_t(k)]);
+    launch_latch_dev(g, et, cs);
+    launch_finish(cd, g, d->vn_grid, cs, d->l2w[size_t(k)]);
+    launch_loop_ctl(g, (unsigned long long)h, cs);
+    cudaGraph_t captured;
+    cudaError_t e = cudaStreamEndCapture(cs, &captured);
+    cudaStreamDestroy(cs);
+    if (e != cudaSuccess) {
+        cudaGraphDestroy(graph);
+        return fail(METLDPC_ECUDA, std::string("loop graph capture: ") + cudaGetErrorString(e));
+    }
+    cudaGraphExec_t exec;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return fail(METLDPC_ECUDA, std::string("loop graph instantiate: ") + cudaGetErrorString(e));
+    d->loop_exec[size_t(k)] = exec;
+    *out = exec;
+    return METLDPC_OK;
+}
+
+// The iteration loop of one group: the CUDA graph (one launch, device-side trip count and
+// early exit) unless profiling needs per-iteration events (host-enqueued loop).
+metldpc_status group_loop(metldpc_decoder d, const GroupJob& j, int N) {
+    if (d->use_graph && !d->profiling) {
+        cudaGraphExec_t exec;
+        metldpc_status st = loop_graph(d, j.k, &exec);
+        if (st) return st;
+        CUDA_TRY(cudaGraphLaunch(exec, j.s));
+        const size_t per_iter = d->cn_classes.size() + 3;
+        d->prof.launches += int64_t(per_iter) * N;      // upper bound (the loop may stop early)
+        d->prof.cn_launches += N;
+        d->prof.vn_launches += N;
+        d->prof.cn_lane_iters += int64_t(j.nb) * N;
+        return METLDPC_OK;
+    }
+    for (int l = 1; l <= N; ++l) group_iter(d, j, l);
+    return METLDPC_OK;
+}
+
 // Decodes up to K groups concurrently: forked from stream `s` onto the workspace streams,
 // iterations interleaved group by group, joined back into `s`.
 metldpc_status decode_round(metldpc_decoder d, std::vector<GroupJob>& jobs, int N, cudaStream_t s) {
@@ -272,8 +343,8 @@ metldpc_status decode_round(metldpc_decoder d, std::vector<GroupJob>& jobs, int 
     if (jobs.size() == 1) {
         jobs[0].s = s;
         if (jobs[0].ready) CUDA_TRY(cudaStreamWaitEvent(s, jobs[0].ready, 0));
-        if ((st = group_begin(d, jobs[0]))) return st;
-        for (int l = 1; l <= N; ++l) group_iter(d, jobs[0], l);
+        if ((st = group_begin(d, jobs[0], N))) return st;
+        if ((st = group_loop(d, jobs[0], N))) return st;
         if ((st = group_end(d, jobs[0], N))) return st;
         if (jobs[0].done) CUDA_TRY(cudaEventRecord(jobs[0].done, s));
         return METLDPC_OK;
@@ -283,10 +354,15 @@ metldpc_status decode_round(metldpc_decoder d, std::vector<GroupJob>& jobs, int 
         j.s = d->gs[size_t(j.k)];
         CUDA_TRY(cudaStreamWaitEvent(j.s, d->fork_ev[0], 0));
         if (j.ready) CUDA_TRY(cudaStreamWaitEvent(j.s, j.ready, 0));
-        if ((st = group_begin(d, j))) return st;
+        if ((st = group_begin(d, j, N))) return st;
     }
-    for (int l = 1; l <= N; ++l)
-        for (auto& j : jobs) group_iter(d, j, l);
+    if (d->use_graph && !d->profiling) {
+        for (auto& j : jobs)
+            if ((st = group_loop(d, j, N))) return st;
+    } else {
+        for (int l = 1; l <= N; ++l)
+            for (auto& j : jobs) group_iter(d, j, l);
+    }
     for (auto& j : jobs) {
         if ((st = group_end(d, j, N))) return st;
         if (j.done) CUDA_TRY(cudaEventRecord(j.done, j.s));
@@ -443,6 +519,11 @@ metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, cons
         }
         cudaGetLastError();
     }
+    d->loop_exec.assign(size_t(d->K), nullptr);
+    {
+        const char* e = std::getenv("METLDPC_GRAPH");
+        d->use_graph = (e && *e == '0') ? 0 : 1;
+    }
     if (d->K > 1) {
         d->gs.resize(size_t(d->K));
         d->join_ev.resize(size_t(d->K));
@@ -490,6 +571,8 @@ void metldpc_decoder_destroy(metldpc_decoder d) {
         dfree(w.conv);
         dfree(w.done);
     }
+    for (auto ex : d->loop_exec)
+        if (ex) cudaGraphExecDestroy(ex);
     for (auto st : d->gs) cudaStreamDestroy(st);
     for (auto e : d->join_ev) cudaEventDestroy(e);
     for (auto e : d->fork_ev) cudaEventDestroy(e);

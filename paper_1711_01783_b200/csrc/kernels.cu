@@ -110,7 +110,21 @@ struct CnCtl {
     int check;   // test the syndrome of iteration l-1 (reads L^{l-1}, degree-1 bits[rpar])
     int first;   // l == 1: r^0 = 0 (not read)
     int rpar, wpar;
+    int dev;     // 1: take l from Group::iter (CUDA-graph loop); check = et && l >= 2
+    int et;
 };
+
+// Resolves the iteration controls of a CN launch (host-given or device-driven).
+__device__ __forceinline__ CnCtl cn_ctl(CnCtl k, const Group& g) {
+    if (k.dev) {
+        const int l = *reinterpret_cast<volatile int*>(g.iter);
+        k.first = (l == 1);
+        k.check = k.et && l >= 2;
+        k.rpar = (l - 1) & 1;
+        k.wpar = l & 1;
+    }
+    return k;
+}
 
 constexpr int kCnThreads = 512;   // 2 CTAs x 16 warps per SM (the replicated table is 100 KB)
 
@@ -326,7 +340,7 @@ template <int NA>
 __host__ __device__ constexpr int cn_tile_min_blocks() { return NA <= 4 ? 2 : 1; }   // NA > 4: 128 registers
 
 template <int RULE, int NA, int ND>
-__global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_tile(CodeDev cd, Group g, CnCtl k,
+__global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_tile(CodeDev cd, Group g, CnCtl karg,
                                                                                   int begin, int count, int ts) {
     using PT = PhiT<RULE>;
     constexpr int LPT = (NA <= 4) ? 2 : 1;     // lanes per thread
@@ -336,6 +350,7 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
     extern __shared__ __align__(16) char smem[];
     __shared__ uint32_t s_unsat[2], s_act[2];
     if (*reinterpret_cast<volatile int*>(g.done)) return;
+    const CnCtl k = cn_ctl(karg, g);
     load_phi_table<RULE>(smem, cd.phi);
     if (threadIdx.x < 2) { s_unsat[threadIdx.x] = 0u; s_act[threadIdx.x] = g.act[threadIdx.x]; }
     __syncthreads();
@@ -475,11 +490,12 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
 // 17..32 (rare in MET ensembles); one CN x one 32-lane chunk per warp item, run-time
 // degree, arrays in local memory.  Same arithmetic (N1).
 template <int RULE>
-__global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group g, CnCtl k, int begin, int count) {
+__global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group g, CnCtl karg, int begin, int count) {
     using PT = PhiT<RULE>;
     extern __shared__ __align__(16) char smem[];
     __shared__ uint32_t s_unsat[4], s_act[4];
     if (*reinterpret_cast<volatile int*>(g.done)) return;
+    const CnCtl k = cn_ctl(karg, g);
     load_phi_table<RULE>(smem, cd.phi);
     if (threadIdx.x < g.C) { s_unsat[threadIdx.x] = 0u; s_act[threadIdx.x] = g.act[threadIdx.x]; }
     __syncthreads();
@@ -689,6 +705,38 @@ __global__ void k_latch(Group g, int l, int final_) {
     if (threadIdx.x == 0) *g.done = s_any ? 0 : 1;
 }
 
+// Graph-loop versions: latch the lanes converged at l - 1 after CN pass l (ET), and
+// advance l, leaving the WHILE condition = (l <= N && some lane still iterating).
+__global__ void k_latch_dev(Group g, int et) {
+    const int l = *reinterpret_cast<volatile int*>(g.iter);
+    if (!et || l < 2) return;
+    const int c = threadIdx.x;
+    __shared__ int s_any;
+    if (threadIdx.x == 0) s_any = 0;
+    __syncthreads();
+    if (c < g.C) {
+        const uint32_t a = g.act[c], u = g.unsat[c];
+        const uint32_t ok = a & ~u;
+        for (int b = 0; b < 32; ++b)
+            if ((ok >> b) & 1u) {
+                g.iters[c * 32 + b] = l - 1;
+                g.conv[c * 32 + b] = 1;
+            }
+        const uint32_t na = a & u;
+        g.act[c] = na;
+        g.unsat[c] = 0u;
+        if (na) atomicOr(&s_any, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *g.done = s_any ? 0 : 1;
+}
+
+__global__ void k_loop_ctl(Group g, cudaGraphConditionalHandle h) {
+    const int l = *g.iter + 1;
+    *g.iter = l;
+    cudaGraphSetConditional(h, (l <= *g.maxit && !*reinterpret_cast<volatile int*>(g.done)) ? 1u : 0u);
+}
+
 // ------------------------------------------------------------------ group init (a1)
 
 // llr [nb][n] frame-major -> lam_a / L / lam1 [slot][B]: 32 VNs x 32 lanes tile transposed
@@ -740,7 +788,11 @@ __global__ void __launch_bounds__(256) k_pack_syndrome(CodeDev cd, Group g, cons
     if (j < cd.m) g.synd_t[size_t(__ldg(cd.cn_new + j)) * g.C + c] = mine;
 }
 
-__global__ void k_init_ctl(Group g, int nb) {
+__global__ void k_init_ctl(Group g, int nb, int N) {
+    if (threadIdx.x == 0) {
+        *g.iter = 1;
+        *g.maxit = N;
+    }
     __shared__ int s_any;
     if (threadIdx.x == 0) s_any = 0;
     __syncthreads();
@@ -981,7 +1033,13 @@ void launch_pack_syndrome(const CodeDev& cd, const Group& g, const uint32_t* syn
     k_pack_syndrome<<<unsigned((items + 7) / 8), 256, 0, s>>>(cd, g, synd, nb);
 }
 
-void launch_init_ctl(const Group& g, int nb, cudaStream_t s) { k_init_ctl<<<1, 128, 0, s>>>(g, nb); }
+void launch_init_ctl(const Group& g, int nb, int N, cudaStream_t s) { k_init_ctl<<<1, 128, 0, s>>>(g, nb, N); }
+
+void launch_latch_dev(const Group& g, bool et, cudaStream_t s) { k_latch_dev<<<1, 32, 0, s>>>(g, et ? 1 : 0); }
+
+void launch_loop_ctl(const Group& g, unsigned long long cond_handle, cudaStream_t s) {
+    k_loop_ctl<<<1, 1, 0, s>>>(g, cudaGraphConditionalHandle(cond_handle));
+}
 
 // Optional persisting-L2 window over the group's L / accumulator rows (set by the decoder
 // when the device supports it).
@@ -1008,7 +1066,7 @@ static cudaError_t launch_with_window(void* f, dim3 grid, dim3 block, void** arg
 
 void launch_cn(const CodeDev& cd, const Group& g, int rule, int D, int nd, int begin, int count, int ts, int grid,
                int l, bool check, cudaStream_t s, const L2Window& w) {
-    CnCtl k{check ? 1 : 0, l == 1 ? 1 : 0, (l - 1) & 1, l & 1};
+    CnCtl k{check ? 1 : 0, l == 1 ? 1 : 0, (l - 1) & 1, l & 1, l == 0 ? 1 : 0, check ? 1 : 0};
     void* f = cn_kernel(rule, D, nd);
     if (D < 0) {
         void* args[] = {const_cast<CodeDev*>(&cd), const_cast<Group*>(&g), &k, &begin, &count};

@@ -26,6 +26,8 @@ struct Group {
     int32_t* iters;    // [B]
     uint8_t* conv;     // [B]
     int32_t* done;     // [1]  all lanes latched
+    int32_t* iter;     // [1]  current iteration l (graph-driven loop; 1-based)
+    int32_t* maxit;    // [1]  N of the running decode
 };
 
 struct CodeDev {
@@ -60,7 +62,12 @@ int finish_blocks_per_sm();
 
 void launch_scatter(const CodeDev& cd, const Group& g, const float* llr, int nb, cudaStream_t s);
 void launch_pack_syndrome(const CodeDev& cd, const Group& g, const uint32_t* synd, int nb, cudaStream_t s);
-void launch_init_ctl(const Group& g, int nb, cudaStream_t s);
+void launch_init_ctl(const Group& g, int nb, int N, cudaStream_t s);
+// Device-driven iteration control for the CUDA-graph loop (l read from Group::iter).
+void launch_latch_dev(const Group& g, bool et, cudaStream_t s);
+void launch_loop_ctl(const Group& g, unsigned long long cond_handle, cudaStream_t s);
+// l >= 1: iteration given by the host; l == 0: read from Group::iter (graph body), with
+// et telling whether iterations >= 2 test the syndrome.
 void launch_cn(const CodeDev& cd, const Group& g, int rule, int D, int nd, int begin, int count, int ts, int grid,
                int l, bool check, cudaStream_t s, const L2Window& w);
 void launch_finish(const CodeDev& cd, const Group& g, int grid, cudaStream_t s, const L2Window& w);
