@@ -102,6 +102,20 @@ metldpc_status metldpc_code_create(int32_t device, int32_t n, int32_t m, int64_t
                                    const int64_t* vn_ptr, const int64_t* vn_edge,
                                    metldpc_code* out);
 
+/* Code-layout flags of metldpc_code_create_ex. */
+#define METLDPC_CODE_NO_SKIP 1u  /* iterate degree-1 VNs like every other VN: the paper's "without
+                                    skipping" variant (Table 1 left columns).  Their
+                                    messages are then stored and summed (posterior form, R10), so
+                                    n_active = n, iter_edges = edges and n_deg1 = 0; the decoded
+                                    word may differ from the skipping decoder's by the rounding of
+                                    L - r vs lambda (R26). */
+
+/* metldpc_code_create with layout flags (0 = metldpc_code_create; EINVAL on unknown bits). */
+metldpc_status metldpc_code_create_ex(int32_t device, int32_t n, int32_t m, int64_t num_edges,
+                                      const int64_t* cn_ptr, const int32_t* edge_vn,
+                                      const int64_t* vn_ptr, const int64_t* vn_edge,
+                                      uint32_t flags, metldpc_code* out);
+
 /* Same from a MacKay alist text file: "n m", "max_vn max_cn", VN degrees,
  * CN degrees, then n lines of 1-based CN lists and m lines of 1-based VN lists.
  * Edges are numbered in CSR order of the CN lists; the CSC order of a column is the

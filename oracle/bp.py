@@ -18,6 +18,7 @@ _LIB = _DIR / "liboracle_bp.so"
 
 RULE_EXACT = 0
 RULE_PHI_LUT = 1
+NO_SKIP = 0x100   # variant bit: iterate degree-1 VNs too (Table 1 "without skipping")
 R_MAX = 30.0
 
 _lib = None
@@ -53,7 +54,7 @@ def lib():
         _lib.orc_step_f64.restype = C.c_int
         _lib.orc_step_f64.argtypes = [C.c_int] + graph + [P, P, P, P, P, P]
         _lib.orc_graph_sizes.restype = C.c_int
-        _lib.orc_graph_sizes.argtypes = graph + [P, P]
+        _lib.orc_graph_sizes.argtypes = [C.c_int] + graph + [P, P]
         _lib.orc_syndrome.restype = None
         _lib.orc_syndrome.argtypes = [C.c_int, C.c_int, P, P, P, P]
         _lib.orc_llr_from_md_f32.restype = None
@@ -78,11 +79,11 @@ def _graph(code):
     return arrs, [code.n, code.m] + [_p(a) for a in arrs]
 
 
-def graph_sizes(code):
+def graph_sizes(code, no_skip: bool = False):
     keep, g = _graph(code)
     E_it = np.zeros(1, np.int64)
     n_a = np.zeros(1, np.int32)
-    rc = lib().orc_graph_sizes(*g, _p(E_it), _p(n_a))
+    rc = lib().orc_graph_sizes(NO_SKIP if no_skip else 0, *g, _p(E_it), _p(n_a))
     if rc:
         raise ValueError(f"malformed code (rc={rc})")
     return int(E_it[0]), int(n_a[0])
@@ -132,8 +133,10 @@ def syndrome(code, bits: np.ndarray) -> np.ndarray:
 
 
 def decode(code, llr: np.ndarray, synd_words: np.ndarray, max_iter: int, early_term: bool = True,
-           rule: int = RULE_EXACT, prec: int = 32, trace: bool = False, posterior: bool = False):
+           rule: int = RULE_EXACT, prec: int = 32, trace: bool = False, posterior: bool = False,
+           no_skip: bool = False):
     """Decode ONE frame.  prec=32 -> M3 (fp32 replay), prec=64 -> M2 (fp64 definition).
+    no_skip iterates degree-1 VNs too (Table 1 "without skipping", R26).
 
     Returns dict(bits uint8[n], iters, converged, [r_trace, L_trace], [post]).
     """
@@ -145,7 +148,9 @@ def decode(code, llr: np.ndarray, synd_words: np.ndarray, max_iter: int, early_t
     out = {}
     rt = Lt = None
     if trace:
-        E_it, n_a = graph_sizes(code)
+        E_it, n_a = graph_sizes(code, no_skip)
+    if no_skip:
+        rule = rule | NO_SKIP
     if prec == 32:
         lam = np.ascontiguousarray(llr, np.float32)
         if trace:
@@ -174,10 +179,12 @@ def decode(code, llr: np.ndarray, synd_words: np.ndarray, max_iter: int, early_t
     return out
 
 
-def step64(code, llr, synd_words, r_in, L_in, rule: int = RULE_EXACT):
+def step64(code, llr, synd_words, r_in, L_in, rule: int = RULE_EXACT, no_skip: bool = False):
     """One fp64 iteration from (r^{l-1}, L^{l-1}) -> (r^l, L^l)."""
     keep, g = _graph(code)
-    E_it, n_a = graph_sizes(code)
+    E_it, n_a = graph_sizes(code, no_skip)
+    if no_skip:
+        rule = rule | NO_SKIP
     lam = np.ascontiguousarray(llr, np.float64)
     s = np.ascontiguousarray(synd_words, np.uint32)
     ri = np.ascontiguousarray(r_in, np.float64)

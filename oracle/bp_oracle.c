@@ -32,6 +32,8 @@
  *       a tie (exact zero) gives 0 -- "if q_i^l > 1, c_i = 1".
  *   Syndrome test (Step 5): stop at the first l with H c^T = S_B when early
  *       termination is on; otherwise run N iterations and test once.
+ *   Variant ORC_NO_SKIP (Table 1 "without skipping"): degree-1 VNs are iterated
+ *       like the others, so "active" means degree >= 1 in everything above.
  * LLR convention lambda = ln P(0)/P(1) = -ln q^0 (Eq. 1 ratio q = q(1)/q(0)).
  */
 #include <math.h>
@@ -50,6 +52,13 @@ static int phi_j(int rule) { return rule == 0 ? PHI_J_EXACT : PHI_J_LUT; }
 static int phi_nbin(int rule) { return ((PHI_E_HI) - (PHI_E_LO)) << phi_j(rule); }
 
 enum { RULE_EXACT = 0, RULE_PHI_LUT = 1 };
+
+/* Variant bit or-ed into the `rule` argument of the decoders (and the `variant`
+ * argument of orc_graph_sizes): iterate degree-1 VNs like every other VN -- the
+ * paper's "without skipping" column of Table 1.  A degree-1 VN then
+ * keeps a message r and a posterior L = lambda + r like any VN (Eq. 4/5), and
+ * its CN input is the extrinsic L - r (R26). */
+#define ORC_NO_SKIP 0x100
 
 /* ------------------------------------------------------------------ phi */
 
@@ -174,7 +183,9 @@ typedef struct {
 } graph_t;
 
 static int graph_build(graph_t* g, int n, int m, const int64_t* cn_ptr, const int32_t* edge_vn,
-                       const int64_t* vn_ptr, const int64_t* vn_edge) {
+                       const int64_t* vn_ptr, const int64_t* vn_edge, int variant) {
+    /* a VN is iterated ("active") if its degree is >= 2, or >= 1 without skipping */
+    const int min_act = (variant & ORC_NO_SKIP) ? 1 : 2;
     memset(g, 0, sizeof(*g));
     g->n = n; g->m = m; g->cn_ptr = cn_ptr; g->edge_vn = edge_vn; g->vn_ptr = vn_ptr; g->vn_edge = vn_edge;
     g->E = cn_ptr[m];
@@ -189,7 +200,7 @@ static int graph_build(graph_t* g, int n, int m, const int64_t* cn_ptr, const in
     for (int v = 0; v < n; ++v) {
         if (g->vdeg[v] == 0) return -2;                      /* degree-0 VN: rejected */
         if (vn_ptr[v + 1] - vn_ptr[v] != g->vdeg[v]) return -3; /* CSR/CSC mismatch */
-        g->vn_act[v] = (g->vdeg[v] >= 2) ? g->n_a++ : -1;
+        g->vn_act[v] = (g->vdeg[v] >= min_act) ? g->n_a++ : -1;
     }
     g->act_vn = malloc((size_t)(g->n_a > 0 ? g->n_a : 1) * sizeof(int32_t));
     for (int v = 0; v < n; ++v) if (g->vn_act[v] >= 0) g->act_vn[g->vn_act[v]] = v;
@@ -198,7 +209,7 @@ static int graph_build(graph_t* g, int n, int m, const int64_t* cn_ptr, const in
         if (cn_ptr[j + 1] - cn_ptr[j] > g->max_cdeg) g->max_cdeg = (int)(cn_ptr[j + 1] - cn_ptr[j]);
     g->E_it = 0;
     for (int64_t e = 0; e < g->E; ++e)
-        g->act_id[e] = (g->vdeg[edge_vn[e]] >= 2) ? g->E_it++ : -1;
+        g->act_id[e] = (g->vdeg[edge_vn[e]] >= min_act) ? g->E_it++ : -1;
     return 0;
 }
 
@@ -206,10 +217,10 @@ static void graph_free(graph_t* g) {
     free(g->vdeg); free(g->act_id); free(g->vn_act); free(g->act_vn);
 }
 
-int orc_graph_sizes(int n, int m, const int64_t* cn_ptr, const int32_t* edge_vn,
+int orc_graph_sizes(int variant, int n, int m, const int64_t* cn_ptr, const int32_t* edge_vn,
                     const int64_t* vn_ptr, const int64_t* vn_edge, int64_t* E_it, int32_t* n_a) {
     graph_t g;
-    int rc = graph_build(&g, n, m, cn_ptr, edge_vn, vn_ptr, vn_edge);
+    int rc = graph_build(&g, n, m, cn_ptr, edge_vn, vn_ptr, vn_edge, variant);
     if (rc == 0) { *E_it = g.E_it; *n_a = g.n_a; }
     graph_free(&g);
     return rc;
@@ -323,7 +334,8 @@ int orc_decode_f32(int rule, int n, int m, const int64_t* cn_ptr, const int32_t*
                    uint8_t* bits_out, int32_t* iters_out, uint8_t* conv_out,
                    float* r_trace, float* L_trace) {
     graph_t g;
-    int rc = graph_build(&g, n, m, cn_ptr, edge_vn, vn_ptr, vn_edge);
+    int rc = graph_build(&g, n, m, cn_ptr, edge_vn, vn_ptr, vn_edge, rule);
+    rule &= 0xff;
     if (rc) { graph_free(&g); return rc; }
     memset(bits_out, 0, (size_t)n);
     if (!all_finite32(lam, n)) { *iters_out = -1; *conv_out = 0; graph_free(&g); return 0; }
@@ -412,7 +424,8 @@ int orc_decode_f64(int rule, int n, int m, const int64_t* cn_ptr, const int32_t*
                    uint8_t* bits_out, int32_t* iters_out, uint8_t* conv_out,
                    double* r_trace, double* L_trace, double* post_out /*[n] or NULL*/) {
     graph_t g;
-    int rc = graph_build(&g, n, m, cn_ptr, edge_vn, vn_ptr, vn_edge);
+    int rc = graph_build(&g, n, m, cn_ptr, edge_vn, vn_ptr, vn_edge, rule);
+    rule &= 0xff;
     if (rc) { graph_free(&g); return rc; }
     memset(bits_out, 0, (size_t)n);
     for (int i = 0; i < n; ++i)
@@ -454,7 +467,8 @@ int orc_step_f64(int rule, int n, int m, const int64_t* cn_ptr, const int32_t* e
                  const double* lam, const uint32_t* synd, const double* r_in, const double* L_in,
                  double* r_out, double* L_out) {
     graph_t g;
-    int rc = graph_build(&g, n, m, cn_ptr, edge_vn, vn_ptr, vn_edge);
+    int rc = graph_build(&g, n, m, cn_ptr, edge_vn, vn_ptr, vn_edge, rule);
+    rule &= 0xff;
     if (rc) { graph_free(&g); return rc; }
     double* rho = calloc((size_t)n, 8);
     cn_phase64(&g, rule, lam, synd, r_in, L_in, r_out, rho);

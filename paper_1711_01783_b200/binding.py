@@ -20,6 +20,7 @@ LIB_PATH = Path(os.environ["METLDPC_LIB"]) if os.environ.get("METLDPC_LIB") else
 
 OK, EINVAL, EFORMAT, ENOMEM, ECUDA, EUNSUPPORTED = range(6)
 RULE_EXACT, RULE_PHI_LUT = 0, 1
+CODE_NO_SKIP = 1
 
 _lib = None
 
@@ -57,6 +58,8 @@ SYMBOLS = {
     # name: (restype, argtypes)
     "metldpc_code_create": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "metldpc_code_create_ex": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_void_p, C.c_uint32, C.POINTER(C.c_void_p)]),
     "metldpc_code_load_alist": (C.c_int, [C.c_int32, C.c_char_p, C.POINTER(C.c_void_p)]),
     "metldpc_code_check": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.POINTER(CodeInfo)]),
@@ -129,6 +132,13 @@ def metldpc_code_create(device, n, m, num_edges, cn_ptr, edge_vn, vn_ptr, vn_edg
     h = C.c_void_p()
     _check(lib().metldpc_code_create(device, n, m, num_edges, _ptr(cn_ptr), _ptr(edge_vn), _ptr(vn_ptr),
                                      _ptr(vn_edge), C.byref(h)), "metldpc_code_create")
+    return h
+
+
+def metldpc_code_create_ex(device, n, m, num_edges, cn_ptr, edge_vn, vn_ptr, vn_edge, flags):
+    h = C.c_void_p()
+    _check(lib().metldpc_code_create_ex(device, n, m, num_edges, _ptr(cn_ptr), _ptr(edge_vn), _ptr(vn_ptr),
+                                        _ptr(vn_edge), int(flags), C.byref(h)), "metldpc_code_create_ex")
     return h
 
 
@@ -239,14 +249,17 @@ class Code:
     """H on a device (immutable).  ``code`` is any object with n, m, cn_ptr, edge_vn,
     vn_ptr, vn_edge numpy arrays (e.g. synth.codes.Code)."""
 
-    def __init__(self, code=None, device: int = 0, alist: str | None = None):
+    def __init__(self, code=None, device: int = 0, alist: str | None = None, no_skip: bool = False):
         import numpy as np
         if alist is not None:
+            if no_skip:
+                raise ValueError("no_skip needs the CSR/CSC arrays (metldpc_code_create_ex)")
             self.h = metldpc_code_load_alist(device, alist)
         else:
             self._keep = [np.ascontiguousarray(code.cn_ptr, np.int64), np.ascontiguousarray(code.edge_vn, np.int32),
                           np.ascontiguousarray(code.vn_ptr, np.int64), np.ascontiguousarray(code.vn_edge, np.int64)]
-            self.h = metldpc_code_create(device, code.n, code.m, int(self._keep[1].size), *self._keep)
+            self.h = metldpc_code_create_ex(device, code.n, code.m, int(self._keep[1].size), *self._keep,
+                                            CODE_NO_SKIP if no_skip else 0)
             del self._keep
         self.info = metldpc_code_info(self.h)
         self.n, self.m = self.info.n, self.info.m

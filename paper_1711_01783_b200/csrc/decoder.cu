@@ -381,11 +381,18 @@ extern "C" {
 metldpc_status metldpc_code_create(int32_t device, int32_t n, int32_t m, int64_t num_edges, const int64_t* cn_ptr,
                                    const int32_t* edge_vn, const int64_t* vn_ptr, const int64_t* vn_edge,
                                    metldpc_code* out) {
+    return metldpc_code_create_ex(device, n, m, num_edges, cn_ptr, edge_vn, vn_ptr, vn_edge, 0u, out);
+}
+
+metldpc_status metldpc_code_create_ex(int32_t device, int32_t n, int32_t m, int64_t num_edges, const int64_t* cn_ptr,
+                                      const int32_t* edge_vn, const int64_t* vn_ptr, const int64_t* vn_edge,
+                                      uint32_t flags, metldpc_code* out) {
     if (!out) return fail(METLDPC_EINVAL, "out is NULL");
     *out = nullptr;
+    if (flags & ~uint32_t(METLDPC_CODE_NO_SKIP)) return fail(METLDPC_EINVAL, "unknown code flags");
     metldpc_code c = new (std::nothrow) metldpc_code_s();
     if (!c) return fail(METLDPC_ENOMEM, "host allocation");
-    metldpc_status s = build_layout(n, m, num_edges, cn_ptr, edge_vn, vn_ptr, vn_edge, &c->host);
+    metldpc_status s = build_layout(n, m, num_edges, cn_ptr, edge_vn, vn_ptr, vn_edge, &c->host, flags);
     if (s == METLDPC_OK) s = check_device(device, &c->num_sms);
     if (s) {
         delete c;

@@ -29,7 +29,7 @@ metldpc_status fail(metldpc_status s, const std::string& msg) {
 
 metldpc_status build_layout(int32_t n, int32_t m, int64_t E, const int64_t* cn_ptr,
                             const int32_t* edge_vn, const int64_t* vn_ptr, const int64_t* vn_edge,
-                            HostLayout* out) {
+                            HostLayout* out, uint32_t flags) {
     if (n <= 0 || m < 0) return fail(METLDPC_EINVAL, "n must be > 0 and m >= 0");
     if (E < 0 || E >= (int64_t(1) << 31)) return fail(METLDPC_EUNSUPPORTED, "num_edges must be in [0, 2^31)");
     if (!cn_ptr || !vn_ptr || (E > 0 && (!edge_vn || !vn_edge)))
@@ -79,13 +79,16 @@ metldpc_status build_layout(int32_t n, int32_t m, int64_t E, const int64_t* cn_p
                                                      std::to_string(edge_vn[e]));
             }
     }
+    // Degree-1 VNs are skipped during iterations unless METLDPC_CODE_NO_SKIP asks for
+    // the paper's "without skipping" variant (Table 1 left columns): then every VN is iterated.
+    const int32_t min_act = (flags & METLDPC_CODE_NO_SKIP) ? 1 : 2;
     HostLayout& L = *out;
     L = HostLayout();
     L.n = n; L.m = m; L.E = E;
     L.vmap.assign(n, 0);
     int32_t n_a = 0;
     for (int32_t v = 0; v < n; ++v) {
-        if (deg[v] >= 2) { L.vmap[v] = n_a++; L.act_vn.push_back(v); }
+        if (deg[v] >= min_act) { L.vmap[v] = n_a++; L.act_vn.push_back(v); }
         L.max_vn_deg = std::max(L.max_vn_deg, deg[v]);
     }
     L.n_a = n_a;
@@ -93,7 +96,7 @@ metldpc_status build_layout(int32_t n, int32_t m, int64_t E, const int64_t* cn_p
     std::vector<int32_t> canon(E, -1);
     int64_t tc = 0;
     for (int64_t e = 0; e < E; ++e)
-        if (deg[edge_vn[e]] >= 2) canon[e] = int32_t(tc++);
+        if (deg[edge_vn[e]] >= min_act) canon[e] = int32_t(tc++);
     // CN relabelling by degree class (stable): key 2D + nd for D <= 16, nd <= 1; else generic
     std::vector<int32_t> cnd(m, 0);
     for (int32_t j = 0; j < m; ++j) {
@@ -101,7 +104,7 @@ metldpc_status build_layout(int32_t n, int32_t m, int64_t E, const int64_t* cn_p
         if (d > kMaxCnDeg)
             return fail(METLDPC_EUNSUPPORTED, "CN " + std::to_string(j) + " has degree " + std::to_string(d) +
                                                   " > " + std::to_string(kMaxCnDeg));
-        for (int64_t e = cn_ptr[j]; e < cn_ptr[j + 1]; ++e) cnd[j] += (deg[edge_vn[e]] == 1);
+        for (int64_t e = cn_ptr[j]; e < cn_ptr[j + 1]; ++e) cnd[j] += (deg[edge_vn[e]] < min_act);
     }
     const int generic_key = 2 * (kMaxUnrolledCnDeg + 1);
     auto cls_key = [&](int32_t j) {
@@ -133,7 +136,7 @@ metldpc_status build_layout(int32_t n, int32_t m, int64_t E, const int64_t* cn_p
         L.max_cn_deg = std::max(L.max_cn_deg, int32_t(cn_ptr[j + 1] - cn_ptr[j]));
         for (int64_t e = cn_ptr[j]; e < cn_ptr[j + 1]; ++e) {
             int32_t v = edge_vn[e];
-            if (deg[v] >= 2) {
+            if (deg[v] >= min_act) {
                 act_id[e] = t++;
                 L.a_vn.push_back(L.vmap[v]);
                 L.perm_r.push_back(canon[e]);
@@ -389,7 +392,7 @@ metldpc_status metldpc_code_check(int32_t n, int32_t m, int64_t num_edges, const
                                   const int32_t* edge_vn, const int64_t* vn_ptr, const int64_t* vn_edge,
                                   metldpc_code_info_t* info_out) {
     HostLayout L;
-    metldpc_status s = build_layout(n, m, num_edges, cn_ptr, edge_vn, vn_ptr, vn_edge, &L);
+    metldpc_status s = build_layout(n, m, num_edges, cn_ptr, edge_vn, vn_ptr, vn_edge, &L, 0);
     if (s == METLDPC_OK && info_out) fill_info(L, info_out);
     return s;
 }

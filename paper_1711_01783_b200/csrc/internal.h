@@ -60,7 +60,7 @@ constexpr int kMaxUnrolledCnDeg = 16;
 // Validates the edge-indexed CSR/CSC and builds the layout.  Returns OK/EFORMAT/EUNSUPPORTED.
 metldpc_status build_layout(int32_t n, int32_t m, int64_t E, const int64_t* cn_ptr,
                             const int32_t* edge_vn, const int64_t* vn_ptr, const int64_t* vn_edge,
-                            HostLayout* out);
+                            HostLayout* out, uint32_t flags);
 
 void fill_info(const HostLayout& L, metldpc_code_info_t* info);
 

@@ -12,6 +12,9 @@ structural count of Table 1 exactly at n = 10^6:
 * ``r0.05``: nu = 0.04 x1^2 x2^34 + 0.03 x1^3 x2^34 + 0.93 x3,
   mu = 0.01 x1^8 + 0.01 x1^9 + 0.41 x2^2 x3 + 0.52 x2^3 x3.
   n=10^6: E = 3,480,000, m = 950,000, 930,000 degree-1 VNs, E_it = 2,550,000.
+* ``r0.02`` (R25): nu = 0.02 x1^2 x2^{56|57} + 0.02 x1^3 x2^{56|57} + 0.96 x3,
+  mu = 0.02 x1^5 + 0.6025 x2^2 x3 + 0.3575 x2^3 x3 (inner degree 57 on 37,500 of the 40,000
+  active VNs).  n=10^6: E = 3,337,500, m = 980,000, 960,000 degree-1 VNs, E_it = 2,377,500.
 
 Construction: per edge type, VN sockets are matched to a seeded Fisher-Yates
 shuffle of CN sockets; parallel edges are repaired by random swaps inside the
@@ -128,6 +131,22 @@ def met_counts(family: str, n: int) -> dict:
         inner = {2: k2, 3: k3}               # CNs x2^2 x3 and x2^3 x3
         vn_core = {2: a2, 3: a3}
         inner_per_vn = 34
+    elif family == "r0.02":
+        # Table 1 rate-0.02 column: E_it = 2.3775 n, n_1 = 0.96 n.
+        a = int(round(0.04 * n))
+        a3 = a // 2
+        a2 = a - a3
+        n1 = n - a
+        m = n - int(round(0.02 * n))
+        t2 = int(round(2.3775 * n)) - (2 * a2 + 3 * a3)
+        lo, n_hi = divmod(t2, a)
+        k3 = t2 - 2 * n1
+        k2 = n1 - k3
+        if k3 < 0 or k2 < 0 or m - n1 <= 0:
+            raise ValueError("r0.02 stand-in infeasible at this n")
+        inner = {2: k2, 3: k3}
+        vn_core = {2: a2, 3: a3}
+        inner_per_vn = np.concatenate([np.full(n_hi, lo + 1), np.full(a - n_hi, lo)])
     else:
         raise ValueError(f"unknown family {family!r}")
     core = m - n1
@@ -137,7 +156,7 @@ def met_counts(family: str, n: int) -> dict:
     return {"n": n, "m": m, "a2": a2, "a3": a3, "n1": n1, "core": core,
             "core_deg": {lo: core - n_hi, lo + 1: n_hi} if n_hi else {lo: core},
             "inner": inner, "vn_core": vn_core, "inner_per_vn": inner_per_vn,
-            "edges": e1 + inner_per_vn * (a2 + a3) + n1}
+            "edges": e1 + int(np.sum(np.broadcast_to(inner_per_vn, (a2 + a3,)))) + n1}
 
 
 def _match(rng, vn_sock: np.ndarray, cn_sock: np.ndarray, m: int):

@@ -118,6 +118,32 @@ def test_c1_messages_every_iteration(c1, rule):
             assert np.array_equal(L.view(np.uint32), traces[i]["L_trace"][l - 1].view(np.uint32)), (l, i)
 
 
+@pytest.mark.parametrize("rule", RULES)
+def test_no_skip_variant_bit_exact(c1, rule):
+    """Table 1 "without skipping" (METLDPC_CODE_NO_SKIP, R26): degree-1 VNs are
+    iterated, every inner CN becomes a (4,0) class; bits/iterations/flags bit-exact against
+    the oracle's no-skip replay, and messages of every edge bit-exact after 7 iterations."""
+    code, _ = c1
+    h = B.Code(code, no_skip=True)
+    assert (h.info.n_active, h.info.n_deg1, h.info.iter_edges) == (code.n, 0, code.num_edges)
+    fr = _frames(code, [(0.161, 4), (0.2, 4), (0.3, 4), (0.5, 4)])
+    llr = _llr_oracle(fr)
+    dec, bits, iters, conv = _gpu_decode(h, llr, fr["synd"], rule, 100)
+    nconv = 0
+    for i in range(len(llr)):
+        o = bp.decode(code, llr[i], fr["synd"][i], 100, early_term=True, rule=rule, prec=32, no_skip=True)
+        _assert_frame_equal(code, o, bits[i], iters[i], conv[i], f"frame {i}")
+        nconv += o["converged"]
+    assert 4 <= nconv < len(llr)
+    dec = B.Decoder(h, len(llr), rule=rule, max_iter=7, early_term=False)
+    dec.decode(torch.from_numpy(llr).cuda(), torch.from_numpy(fr["synd"].view(np.int32)).cuda())
+    for i in (0, 9):
+        o = bp.decode(code, llr[i], fr["synd"][i], 7, early_term=False, rule=rule, prec=32, trace=True, no_skip=True)
+        r, L = dec.dump(i)
+        assert np.array_equal(r.view(np.uint32), o["r_trace"][-1].view(np.uint32)), i
+        assert np.array_equal(L.view(np.uint32), o["L_trace"][-1].view(np.uint32)), i
+
+
 @pytest.mark.parametrize("et", [True, False])
 def test_batch_lane_and_group_invariance(c1, et):
     """S:220 / R12: a frame's result does not depend on batch size, lane or group size."""
@@ -285,6 +311,29 @@ def test_c4_rate005_full_size_sampled_lane():
     i = 41
     lam = bp.llr_from_md_f32(fr["v"][i], fr["xnorm"][i], 0.076)
     o = bp.decode(code, lam, fr["synd"][i], 150, rule=B.RULE_EXACT, prec=32)
+    _assert_frame_equal(code, o, bits[i], iters[i], conv[i], f"lane {i}")
+    assert (iters > 0).all()
+
+
+def test_c6_rate002_full_size_sampled_lane():
+    """Rate-0.02 column of Table 1 (R25 stand-in: E 3,337,500, m 980,000,
+    960,000 degree-1 VNs, E_it 2,377,500), n = 10^6, SNR 0.029, N = 200:
+    active VNs of degree 59-60 and classes (2,1), (3,1), (5,0); one sampled lane
+    replayed by the oracle bit-exactly."""
+    code = make_met_code("r0.02", 10 ** 6)
+    h = B.Code(code)
+    assert (h.info.edges, h.info.iter_edges, h.info.m) == (3337500, 2377500, 980000)
+    nf = 64
+    fr = gen_batch(code, 0.029, 0, range(nf))
+    dec = B.Decoder(h, nf, rule=B.RULE_EXACT, max_iter=200)
+    llr_d = dec.llr_from_md(torch.from_numpy(fr["v"]).cuda(), torch.from_numpy(fr["xnorm"]).cuda(), 0.029)
+    bits, iters, conv = dec.decode(llr_d, torch.from_numpy(fr["synd"].view(np.int32)).cuda())
+    bits = bits.cpu().numpy().view(np.uint32)
+    iters = iters.cpu().numpy()
+    conv = conv.cpu().numpy()
+    i = 17
+    lam = bp.llr_from_md_f32(fr["v"][i], fr["xnorm"][i], 0.029)
+    o = bp.decode(code, lam, fr["synd"][i], 200, rule=B.RULE_EXACT, prec=32)
     _assert_frame_equal(code, o, bits[i], iters[i], conv[i], f"lane {i}")
     assert (iters > 0).all()
 

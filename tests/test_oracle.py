@@ -146,6 +146,38 @@ def test_tree_codes_equal_bitwise_map(seed):
         assert (o3["bits"][clear] == (ref[clear] < 0)).all()
 
 
+@pytest.mark.parametrize("seed", range(6))
+def test_tree_codes_no_skip_equal_bitwise_map(seed):
+    """The "without skipping" variant (Table 1 left columns, R26) is the same BP
+    (a degree-1 VN's extrinsic message is lambda: Eq. (4) with an empty sum), so on a
+    cycle-free graph it also reaches the brute-force bitwise MAP posterior."""
+    rng = np.random.default_rng(300 + seed)
+    tc = tree_code(rng, n_cn=int(rng.integers(2, 6)))
+    assert (tc.vn_degree == 1).any()
+    lam = rng.normal(0.4, 1.5, tc.n)
+    s = rng.integers(0, 2, tc.m)
+    ref = brute.bitwise_map(tc.dense(), s, lam)
+    o = bp.decode(tc, lam, pack_bits(s), 2 * tc.m + 2, early_term=False, prec=64, posterior=True, no_skip=True)
+    assert np.allclose(o["post"], ref, atol=1e-9, rtol=1e-9)
+    E_it, n_a = bp.graph_sizes(tc, no_skip=True)
+    assert (E_it, n_a) == (tc.num_edges, tc.n)
+
+
+def test_no_skip_equals_skip_in_fp64(code_c1):
+    """M2: skipping degree-1 VNs changes the work, not the messages: every
+    active-edge message and active posterior agree to rounding, and the degree-1 edges'
+    stored messages are the CN outputs the skipping decoder folds into its decisions."""
+    f = gen_frame(code_c1, 0.2, 5, 0)
+    lam = bp.llr_from_md_f64(f["v"], f["xnorm"], 0.2)
+    a = bp.decode(code_c1, lam, f["synd"], 25, early_term=False, prec=64, trace=True)
+    b = bp.decode(code_c1, lam, f["synd"], 25, early_term=False, prec=64, trace=True, no_skip=True)
+    assert (a["bits"] == b["bits"]).all() and a["iters"] == b["iters"] and a["converged"] == b["converged"]
+    act_e = np.nonzero(code_c1.vn_degree[code_c1.edge_vn] >= 2)[0]
+    act_v = np.nonzero(code_c1.vn_degree >= 2)[0]
+    assert np.allclose(b["r_trace"][:, act_e], a["r_trace"], rtol=1e-9, atol=1e-9)
+    assert np.allclose(b["L_trace"][:, act_v], a["L_trace"], rtol=1e-9, atol=1e-9)
+
+
 def test_loopy_tiny_codes_vs_ml():
     """S:223 / S:485: on n <= 16 codes, a converged BP output lies in the coset
     and its likelihood never exceeds the block-ML member's; with at most one

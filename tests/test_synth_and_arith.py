@@ -35,7 +35,7 @@ def test_structural_arithmetic_table1(col):
     assert col["total_edges"] - col["ignored_vns"] == col["iter_edges"]
 
 
-@pytest.mark.parametrize("family,idx", [("r0.1", 0), ("r0.05", 1)])
+@pytest.mark.parametrize("family,idx", [("r0.1", 0), ("r0.05", 1), ("r0.02", 2)])
 def test_standin_codes_match_table1(family, idx):
     """The stand-in ensembles reproduce every structural count of Table 1 at n = 10^6."""
     col = T1["columns"][idx]
