@@ -226,6 +226,8 @@ metldpc_status group_begin(metldpc_decoder d, const GroupJob& j, int N) {
     const CodeDev cd = code_dev(d->code, d->cfg.rule);
     const Group g = group_of(d, j.k);
     CUDA_TRY(cudaMemsetAsync(d->ws[size_t(j.k)].ctl + 8, 0, 4 * sizeof(uint32_t), j.s));
+    // r^0 = 0 (Step 2): the CN kernels read r unconditionally (~0.2 % of a decode's traffic)
+    CUDA_TRY(cudaMemsetAsync(g.r, 0, size_t(cd.E_it) * size_t(g.B) * sizeof(float), j.s));
     launch_scatter(cd, g, j.llr, j.nb, j.s);
     launch_pack_syndrome(cd, g, j.synd, j.nb, j.s);
     launch_init_ctl(g, j.nb, N, j.s);

@@ -66,12 +66,20 @@ __device__ __forceinline__ uint32_t one_bits() {
     return c;
 }
 
+// Bit pattern of y clamped to [2^-44, 2^6].  For y >= +0 (or y = |x|) the float order is the
+// order of the bit patterns, so this equals the integer clamp of N2; as FMNMX it folds the
+// |x| of the callers into an operand modifier.  (A NaN, only possible in an invalid frame
+// whose lane is discarded, clamps to 2^-44.)
+__device__ __forceinline__ uint32_t phi_clamp_bits(float y) {
+    return __float_as_uint(fminf(fmaxf(y, __uint_as_float(kPhiLoBits)), __uint_as_float(kPhiHiBits)));
+}
+
 // tabk: 32-bit shared-window address of this lane's table copy minus BIAS (phi_tab_lane).
 template <int RULE>
 __device__ __forceinline__ float phi_dev(uint32_t tabk, float y, uint32_t one) {
     using P = PhiT<RULE>;
     constexpr uint32_t LOW = (1u << (23 - P::J)) - 1u;
-    const uint32_t u = min(max(__float_as_uint(y), kPhiLoBits), kPhiHiBits);
+    const uint32_t u = phi_clamp_bits(y);
     uint32_t e;   // tabk + bin * STRIDE as one IMAD (FMA pipe) after the shift
     asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(e) : "r"(u >> (23 - P::J)), "n"(P::STRIDE), "r"(tabk));
     const float ts = __fsub_rn(__uint_as_float(and_or<LOW>(u, one)), 1.0f);
@@ -108,7 +116,6 @@ __device__ __forceinline__ void load_phi_table(char* smem, const float* phi) {
 
 struct CnCtl {
     int check;   // test the syndrome of iteration l-1 (reads L^{l-1}, degree-1 bits[rpar])
-    int first;   // l == 1: r^0 = 0 (not read)
     int rpar, wpar;
     int dev;     // 1: take l from Group::iter (CUDA-graph loop); check = et && l >= 2
     int et;
@@ -118,7 +125,6 @@ struct CnCtl {
 __device__ __forceinline__ CnCtl cn_ctl(CnCtl k, const Group& g) {
     if (k.dev) {
         const int l = *reinterpret_cast<volatile int*>(g.iter);
-        k.first = (l == 1);
         k.check = k.et && l >= 2;
         k.rpar = (l - 1) & 1;
         k.wpar = l & 1;
@@ -142,7 +148,7 @@ __device__ __forceinline__ uint32_t vn_fix(float o) {
 template <int RULE, int NA, int ND>
 __device__ __forceinline__ uint32_t cn_lane(uint32_t tabk, const float (&Lv)[NA > 0 ? NA : 1],
                                             const float (&ro)[NA > 0 ? NA : 1], float lam, uint32_t sbit,
-                                            uint32_t d1prev, float* pr, float* pla, const int (&offs)[NA > 0 ? NA : 1],
+                                            uint32_t d1prev, float* pr, float* pla, const uint32_t (&offs)[NA > 0 ? NA : 1],
                                             const int* idx, bool act, uint32_t& d1bit) {
     constexpr int D = NA + ND;
     const uint32_t one = one_bits();
@@ -176,12 +182,11 @@ __device__ __forceinline__ uint32_t cn_lane(uint32_t tabk, const float (&Lv)[NA 
         const float mag = fminf(phi_dev<RULE>(tabk, S, one), kRMax);
         const float o = __uint_as_float(__float_as_uint(mag) | ((par ^ xb[s]) & 0x80000000u));
         if (s < NA) {
-            if (act) {
-                __stcs(pr + s * 64, o);
-                // VN sum (Eq. 4); row offsets from registers for small NA, from shared memory otherwise
-                const int ro_s = (NA <= 4) ? offs[s] : idx[s];
-                atomicAdd(reinterpret_cast<unsigned int*>(pla + ro_s + 64), vn_fix(o));
-            }
+            (void)act;   // unpredicated, as in cn_pair
+            __stcs(pr + s * 64, o);
+            // VN sum (Eq. 4); row offsets from registers for small NA, from shared memory otherwise
+            const uint32_t ro_s = (NA <= 4) ? offs[s] : uint32_t(idx[s]);
+            atomicAdd(reinterpret_cast<unsigned int*>(pla + ro_s + 64), vn_fix(o));
         } else {
             d1bit = uint32_t(__fadd_rn(lam, o) < 0.0f);   // Step 5 for VN_b
         }
@@ -226,8 +231,8 @@ template <int RULE>
 __device__ __forceinline__ float2 phi_pair(uint32_t tabk, float y0, float y1, uint32_t one) {
     using P = PhiT<RULE>;
     constexpr uint32_t LOW = (1u << (23 - P::J)) - 1u;
-    const uint32_t u0 = min(max(__float_as_uint(y0), kPhiLoBits), kPhiHiBits);
-    const uint32_t u1 = min(max(__float_as_uint(y1), kPhiLoBits), kPhiHiBits);
+    const uint32_t u0 = phi_clamp_bits(y0);
+    const uint32_t u1 = phi_clamp_bits(y1);
     uint32_t e0, e1;
     asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(e0) : "r"(u0 >> (23 - P::J)), "n"(P::STRIDE), "r"(tabk));
     asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(e1) : "r"(u1 >> (23 - P::J)), "n"(P::STRIDE), "r"(tabk));
@@ -255,8 +260,8 @@ __device__ __forceinline__ float2 phi_pair(uint32_t tabk, float y0, float y1, ui
 template <int RULE, int NA, int ND>
 __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 0 ? NA : 1],
                                          const float2 (&ro)[NA > 0 ? NA : 1], float2 lam, uint2 sbit, uint2 d1prev,
-                                         float* pr, float* pla, const int (&offs)[NA > 0 ? NA : 1], bool act0,
-                                         bool act1, uint2& d1bit) {
+                                         float* pr, float* pla, const uint32_t (&offs)[NA > 0 ? NA : 1],
+                                         uint2& d1bit) {
     constexpr int D = NA + ND;
     const uint32_t one = one_bits();
     const float2 zero2 = make_float2(0.0f, 0.0f);
@@ -298,16 +303,15 @@ __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 
             __uint_as_float(__float_as_uint(fminf(ph.x, kRMax)) | ((par0 ^ xb0[s]) & 0x80000000u)),
             __uint_as_float(__float_as_uint(fminf(ph.y, kRMax)) | ((par1 ^ xb1[s]) & 0x80000000u)));
         if (s < NA) {
+            // Unpredicated: a latched or padding lane's r and accumulator columns are never
+            // read for that lane again (k_finish keeps its L and clears the accumulator), and
+            // full 256-byte rows avoid partial-sector writes.
             const float2 fx = f2fma(o, make_float2(131072.0f, 131072.0f), make_float2(12582912.0f, 12582912.0f));
             unsigned int* pa = reinterpret_cast<unsigned int*>(pla + offs[s] + 64);
-            if (act0) {
-                __stcs(pr + s * 64, o.x);
-                atomicAdd(pa, __float_as_uint(fx.x));          // VN sum (Eq. 4, N3)
-            }
-            if (act1) {
-                __stcs(pr + s * 64 + 32, o.y);
-                atomicAdd(pa + 32, __float_as_uint(fx.y));
-            }
+            __stcs(pr + s * 64, o.x);
+            atomicAdd(pa, __float_as_uint(fx.x));              // VN sum (Eq. 4, N3)
+            __stcs(pr + s * 64 + 32, o.y);
+            atomicAdd(pa + 32, __float_as_uint(fx.y));
         } else {
             const float2 dd = f2add(lam, o);
             d1bit = make_uint2(uint32_t(dd.x < 0.0f), uint32_t(dd.y < 0.0f));   // Step 5 for VN_b
@@ -402,19 +406,20 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
                     }
                 }
                 const int* idx = s_idx + (ab - A0);
-                float* pL = g.L + (c0 * 32 + lane);
-                float* pr = g.r + (size_t(ab) * 64 + c0 * 32 + lane);
+                const uint32_t lo = uint32_t(c0 * 32 + lane);
+                float* pL = g.L + lo;
+                float* pr = g.r + (size_t(ab) * 64 + lo);
                 float Lv[LPT][NAS], ro[LPT][NAS], lam[LPT];
-                int offs[NAS];
+                uint32_t offs[NAS];   // NA <= 4: row offset + lane as one unsigned index (one IMAD.WIDE.U32)
                 uint32_t w[LPT];
 #pragma unroll
                 for (int s = 0; s < NA; ++s) {
                     const int o = idx[s];
-                    if constexpr (NA <= 4) offs[s] = o;
+                    if constexpr (NA <= 4) offs[s] = uint32_t(o) + lo;
 #pragma unroll
                     for (int h = 0; h < LPT; ++h) {
-                        Lv[h][s] = __ldg(pL + o + h * 32);
-                        ro[h][s] = k.first ? 0.0f : __ldcs(pr + s * 64 + h * 32);
+                        Lv[h][s] = (NA <= 4) ? __ldg(g.L + offs[s] + h * 32) : __ldg(pL + o + h * 32);
+                        ro[h][s] = __ldcs(pr + s * 64 + h * 32);   // r^0 = 0: zeroed at group begin
                     }
                 }
                 uint2 wv = make_uint2(0, 0);
@@ -438,8 +443,7 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
                     uint2 d1 = make_uint2(0, 0);
                     const uint2 c2 = cn_pair<RULE, NA, ND>(
                         tabk, L2, r2, make_float2(lam[0], lam[1]), make_uint2((swx >> lane) & 1u, (swy >> lane) & 1u),
-                        make_uint2((wv.x >> lane) & 1u, (wv.y >> lane) & 1u), pr, pL, offs, ((am0 >> lane) & 1u) != 0u,
-                        ((am1 >> lane) & 1u) != 0u, d1);
+                        make_uint2((wv.x >> lane) & 1u, (wv.y >> lane) & 1u), pr, g.L, offs, d1);
                     chk[0] = c2.x;
                     chk[1] = c2.y;
                     b[0] = d1.x;
@@ -452,8 +456,8 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
                     w[h] = (((c ? wv.y : wv.x) >> lane) & 1u);
                     const bool act = (((c ? am1 : am0) >> lane) & 1u) != 0u;
                     b[h] = 0;
-                    chk[h] = cn_lane<RULE, NA, ND>(tabk, Lv[h], ro[h], lam[h], sbit, w[h], pr + h * 32, pL + h * 32, offs,
-                                                   idx, act, b[h]);
+                    chk[h] = cn_lane<RULE, NA, ND>(tabk, Lv[h], ro[h], lam[h], sbit, w[h], pr + h * 32,
+                                                   (NA <= 4 ? g.L : pL) + h * 32, offs, idx, act, b[h]);
                 }
                 }
 #pragma unroll
@@ -522,7 +526,7 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group 
             if (s < na) {
                 const int v = __shfl_sync(FULL, idx, s);
                 const float Lv = __ldg(g.L + size_t(v) * 2 * g.B + off);
-                const float ro = k.first ? 0.0f : __ldcs(g.r + size_t(ab + s) * g.B + off);
+                const float ro = __ldcs(g.r + size_t(ab + s) * g.B + off);
                 x = __fsub_rn(Lv, ro);
                 chk ^= uint32_t(Lv < 0.0f);
             } else {
@@ -1066,7 +1070,7 @@ static cudaError_t launch_with_window(void* f, dim3 grid, dim3 block, void** arg
 
 void launch_cn(const CodeDev& cd, const Group& g, int rule, int D, int nd, int begin, int count, int ts, int grid,
                int l, bool check, cudaStream_t s, const L2Window& w) {
-    CnCtl k{check ? 1 : 0, l == 1 ? 1 : 0, (l - 1) & 1, l & 1, l == 0 ? 1 : 0, check ? 1 : 0};
+    CnCtl k{check ? 1 : 0, (l - 1) & 1, l & 1, l == 0 ? 1 : 0, check ? 1 : 0};
     void* f = cn_kernel(rule, D, nd);
     if (D < 0) {
         void* args[] = {const_cast<CodeDev*>(&cd), const_cast<Group*>(&g), &k, &begin, &count};
