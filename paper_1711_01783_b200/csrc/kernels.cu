@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "internal.h"
@@ -326,6 +327,15 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// One-line L2 prefetch (no registers held; the line is fetched by L2 while the warp computes).
+__device__ __forceinline__ void prefetch_line_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+#ifndef METLDPC_CN_PFL
+#define METLDPC_CN_PFL 0    // CNs of look-ahead for per-lane r / lambda line prefetches into L2
+#endif
+
 #ifndef METLDPC_CN_PAIR
 #define METLDPC_CN_PAIR 1   // two-lane path with packed fp32x2 ops (FADD2 / FFMA2)
 #endif
@@ -393,7 +403,37 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
                 if constexpr (NA > 0) prefetch_l2(g.r + size_t(a_l) * 64, NA * 256);
                 if constexpr (ND > 0) prefetch_l2(g.lam1 + size_t(d_l) * 64, 256);
             }
+            // Exact-degree classes: CN i of the tile owns r rows A0 + i NA .. + NA and lambda row
+            // Q0 + i, so its 128-byte lines are known without metadata.  Lane k prefetches line
+            // k mod LPC of CN (k / LPC) of a round of CPR CNs, PFL CNs ahead of the compute.
+            constexpr int PFL = (LPT == 2 && NA > 0) ? METLDPC_CN_PFL : 0;
+            constexpr int LPC = 2 * NA + 2 * ND, CPR = (LPC > 0 && LPC <= 32) ? 32 / LPC : 1;
+            const char* pf_base = nullptr;
+            size_t pf_step = 0;
+            int pf_cn = 0;
+            bool pf_ok = false;
+            if constexpr (PFL > 0) {
+                const int Q0 = __shfl_sync(FULL, d_l, 0);
+                pf_cn = lane / LPC;
+                const int line = lane % LPC;
+                pf_ok = lane < CPR * LPC;
+                if (line < 2 * NA) {
+                    pf_base = reinterpret_cast<const char*>(g.r + size_t(A0 + pf_cn * NA) * 64) + line * 128;
+                    pf_step = size_t(NA) * 256;
+                } else {
+                    pf_base = reinterpret_cast<const char*>(g.lam1 + size_t(Q0 + pf_cn) * 64) + (line - 2 * NA) * 128;
+                    pf_step = 256;
+                }
+                for (int c = 0; c < PFL; c += CPR)
+                    if (pf_ok && c + pf_cn < nt) prefetch_line_l2(pf_base + size_t(c) * pf_step);
+            }
             for (int i = 0; i < nt; ++i) {
+                if constexpr (PFL > 0) {
+                    if (i % CPR == 0) {
+                        const int c = i + PFL;
+                        if (pf_ok && c + pf_cn < nt) prefetch_line_l2(pf_base + size_t(c) * pf_step);
+                    }
+                }
                 const int ab = __shfl_sync(FULL, a_l, i);
                 const int q0 = __shfl_sync(FULL, d_l, i);
                 const uint32_t swx = __shfl_sync(FULL, sw_l.x, i), swy = __shfl_sync(FULL, sw_l.y, i);
@@ -418,15 +458,29 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
                     if constexpr (NA <= 4) offs[s] = uint32_t(o) + lo;
 #pragma unroll
                     for (int h = 0; h < LPT; ++h) {
+#if defined(METLDPC_EXP_L_LOCAL)   // timing experiment only: L gathers from one row (L1 hits)
+                        Lv[h][s] = __ldg(g.L + lo + s * 4 + h * 32);
+#else
                         Lv[h][s] = (NA <= 4) ? __ldg(g.L + offs[s] + h * 32) : __ldg(pL + o + h * 32);
+#endif
+#if defined(METLDPC_EXP_NO_R)      // timing experiment only: no r reads
+                        ro[h][s] = __uint_as_float(lo * 7u + uint32_t(s));
+#else
                         ro[h][s] = __ldcs(pr + s * 64 + h * 32);   // r^0 = 0: zeroed at group begin
+#endif
                     }
                 }
                 uint2 wv = make_uint2(0, 0);
                 if constexpr (ND > 0) {
                     const float* pl = g.lam1 + (size_t(q0) * 64 + c0 * 32 + lane);
 #pragma unroll
-                    for (int h = 0; h < LPT; ++h) lam[h] = __ldcs(pl + h * 32);
+                    for (int h = 0; h < LPT; ++h) {
+#if defined(METLDPC_EXP_NO_R)
+                        lam[h] = __uint_as_float(lo * 5u + uint32_t(h) + uint32_t(q0));
+#else
+                        lam[h] = __ldcs(pl + h * 32);
+#endif
+                    }
                     if (k.check) wv = __ldg(reinterpret_cast<const uint2*>(g.d1bits) + (size_t(k.rpar) * cd.n_1 + q0));
                 } else {
 #pragma unroll
@@ -480,6 +534,226 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
                     }
                 }
             }
+        }
+    }
+    if (k.check && lane == 0) {
+        if (un0 & am0) atomicOr(&s_unsat[0], un0 & am0);
+        if (un1 & am1) atomicOr(&s_unsat[1], un1 & am1);
+    }
+    __syncthreads();
+    if (k.check && threadIdx.x < 2 && s_unsat[threadIdx.x]) atomicOr(g.unsat + threadIdx.x, s_unsat[threadIdx.x]);
+}
+
+// ------------------------------------------------------------------ TMA-pipelined CN tiles
+
+// Exact-degree classes with 1..4 active slots and <= 1 degree-1 slot (at C3: 97 % of the
+// CNs, all of the inner checks) for 64-lane groups.  Same arithmetic as k_cn_tile (cn_pair),
+// different data movement: every input of a CN arrives in shared memory by TMA while the
+// warp computes the previous CN.  In an exact-degree class CN j owns r rows abase +
+// (j - begin) NA .. + NA and lambda row dbase + (j - begin), and its active VNs' posterior
+// rows are L + a_vn * 128 (256 bytes each); one lane per warp issues 1D bulk copies
+// (cp.async.bulk, no registers held) of those 2 NA + ND rows into a 2-stage ring completing
+// on an mbarrier, so a warp always has the next CN's DRAM and L2 traffic in flight.  The
+// tile's VN row offsets are staged one tile ahead (double buffer) so the producer can run
+// into the next tile.  One CTA per SM shares a single phi table; its warp count is what
+// the rings leave room for.
+constexpr int kPipeStages = 2;
+constexpr int kSmemPerSm = 232448;     // opt-in dynamic shared memory per block (227 KB)
+#ifndef METLDPC_PIPE_L
+#define METLDPC_PIPE_L 0   // 1: the L rows also come by TMA (measured slower: 0.59 vs 0.54 ms at C3)
+#endif
+#ifndef METLDPC_PIPE_LREG
+#define METLDPC_PIPE_LREG 0   // 1: the next CN's L gathers are issued into registers one CN ahead
+#endif
+
+template <int NA, int ND>
+struct PipeCfg {
+    static constexpr int NL = METLDPC_PIPE_L ? NA : 0;                // staged posterior rows
+    static constexpr int STG = (NA + ND + NL) * 256;                  // bytes per stage: r, lambda[, L]
+    static constexpr int IDX = 32 * NA;                               // ints per staged tile
+    static constexpr int WARP_BYTES = 2 * IDX * 4 + kPipeStages * STG + kPipeStages * 8;
+    static constexpr int TAB = (PhiT<METLDPC_RULE_EXACT>::TAB_BYTES > PhiT<METLDPC_RULE_PHI_LUT>::TAB_BYTES)
+                                   ? PhiT<METLDPC_RULE_EXACT>::TAB_BYTES
+                                   : PhiT<METLDPC_RULE_PHI_LUT>::TAB_BYTES;
+    static constexpr int W0 = (kSmemPerSm - TAB - 64) / WARP_BYTES;
+    static constexpr int WMAX = METLDPC_PIPE_LREG ? 24 : 32;          // L prefetch in registers: 80 regs
+    static constexpr int WARPS = W0 > WMAX ? WMAX : W0;
+    static constexpr int THREADS = WARPS * 32;
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// Streams read once per iteration (r, lambda): evict-first, so the L / accumulator rows stay in L2.
+__device__ __forceinline__ void tma_load_1d_ef(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
+template <int RULE, int NA, int ND>
+__global__ void __launch_bounds__(PipeCfg<NA, ND>::THREADS, 1)
+    k_cn_pipe(CodeDev cd, Group g, CnCtl karg, int begin, int count) {
+    using PT = PhiT<RULE>;
+    using PC = PipeCfg<NA, ND>;
+    constexpr int TS = 32;                     // CNs per tile
+    extern __shared__ __align__(128) char smem[];
+    __shared__ uint32_t s_unsat[2], s_act[2];
+    if (*reinterpret_cast<volatile int*>(g.done)) return;
+    const CnCtl k = cn_ctl(karg, g);
+    load_phi_table<RULE>(smem, cd.phi);
+    if (threadIdx.x < 2) { s_unsat[threadIdx.x] = 0u; s_act[threadIdx.x] = g.act[threadIdx.x]; }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    char* wb = smem + PT::TAB_BYTES + warp * PC::WARP_BYTES;
+    int* s_idx = reinterpret_cast<int*>(wb);                         // [2][IDX]
+    char* stage = wb + 2 * PC::IDX * 4;                              // [kPipeStages][STG]
+    const uint32_t stage_a = smem_addr(stage);
+    const uint32_t bar_a = smem_addr(stage + kPipeStages * PC::STG);
+    if (lane == 0) {
+        for (int st = 0; st < kPipeStages; ++st) mbar_init(bar_a + 8 * st, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t tabk = phi_tab_lane<RULE>(smem, lane);
+    const uint32_t am0 = s_act[0], am1 = s_act[1];
+    const int abase = __ldg(cd.cn_aptr + begin);
+    const int dbase = ND ? __ldg(cd.cn_dptr + begin) : 0;
+    const int ntiles = (count + TS - 1) / TS;
+    const int GW = gridDim.x * PC::WARPS;
+    const int gw = blockIdx.x * PC::WARPS + warp;
+    const uint64_t pol = l2_evict_first_policy();
+    auto stage_idx = [&](int tile, int b) {   // VN row offsets (a * 128 floats) of a tile
+        const int jt = tile * TS, nt = min(TS, count - jt);
+        for (int e = lane; e < nt * NA; e += 32) s_idx[b * PC::IDX + e] = __ldg(cd.a_vn + abase + jt * NA + e) * 128;
+    };
+    // producer cursor (tile, index, idx buffer) runs kPipeStages - 1 CNs ahead of the consumer
+    int pt = gw, pi = 0, pb = 0;
+    uint32_t np = 0, nc = 0;
+    auto produce = [&]() {
+        if (pt >= ntiles) return;
+        const int jl = pt * TS + pi;
+        if (lane == 0) {
+            const uint32_t st = np % kPipeStages;
+            const uint32_t bar = bar_a + 8 * st, dst = stage_a + st * PC::STG;
+            mbar_expect_tx(bar, PC::STG);
+            tma_load_1d_ef(dst, g.r + size_t(abase + jl * NA) * 64, NA * 256, bar, pol);
+            if constexpr (ND > 0) tma_load_1d_ef(dst + NA * 256, g.lam1 + size_t(dbase + jl) * 64, 256, bar, pol);
+            if constexpr (PC::NL > 0) {
+                const int* ix = s_idx + pb * PC::IDX + pi * NA;
+#pragma unroll
+                for (int s = 0; s < NA; ++s) tma_load_1d(dst + (NA + ND + s) * 256, g.L + ix[s], 256, bar);
+            }
+        }
+        ++np;
+        if (++pi == min(TS, count - pt * TS)) { pi = 0; pt += GW; pb ^= 1; }
+    };
+    if (gw < ntiles) stage_idx(gw, 0);
+    __syncwarp();
+    for (int st = 0; st < kPipeStages - 1; ++st) produce();
+    uint32_t un0 = 0, un1 = 0;
+    int cb = 0;
+    for (int tile = gw; tile < ntiles; tile += GW, cb ^= 1) {
+        const int jt = tile * TS;                           // class-local index of the tile's first CN
+        const int nt = min(TS, count - jt);
+        const bool on = lane < nt;
+        // the next tile's row offsets: its buffer last held the previous tile, finished
+        if (tile + GW < ntiles) stage_idx(tile + GW, cb ^ 1);
+        const uint2 sw_l = on ? __ldg(reinterpret_cast<const uint2*>(g.synd_t) + (begin + jt + lane)) : make_uint2(0, 0);
+        uint2 wv_l = make_uint2(0, 0);
+        if constexpr (ND > 0)
+            if (k.check && on)
+                wv_l = __ldg(reinterpret_cast<const uint2*>(g.d1bits) + (size_t(k.rpar) * cd.n_1 + dbase + jt + lane));
+        __syncwarp();
+        float2 Lnx[NA];   // METLDPC_PIPE_LREG: L of CN i, gathered during CN i - 1
+        if constexpr (METLDPC_PIPE_LREG && PC::NL == 0) {
+            const int* ix = s_idx + cb * PC::IDX;
+#pragma unroll
+            for (int s = 0; s < NA; ++s) {
+                const uint32_t o = uint32_t(ix[s]) + uint32_t(lane);
+                Lnx[s] = make_float2(__ldg(g.L + o), __ldg(g.L + o + 32));
+            }
+        }
+        for (int i = 0; i < nt; ++i) {
+            produce();
+            const uint32_t st = nc % kPipeStages, ph = (nc / kPipeStages) & 1u;
+            ++nc;
+            const uint32_t swx = __shfl_sync(FULL, sw_l.x, i), swy = __shfl_sync(FULL, sw_l.y, i);
+            uint2 wv = make_uint2(0, 0);
+            if constexpr (ND > 0) {
+                wv.x = __shfl_sync(FULL, wv_l.x, i);
+                wv.y = __shfl_sync(FULL, wv_l.y, i);
+            }
+            const int jl = jt + i;
+            const int* idx = s_idx + cb * PC::IDX + i * NA;
+            uint32_t offs[NA];
+            float2 L2[NA], r2[NA];
+#pragma unroll
+            for (int s = 0; s < NA; ++s) {
+                offs[s] = uint32_t(idx[s]) + uint32_t(lane);
+                if constexpr (PC::NL == 0) {
+                    if constexpr (METLDPC_PIPE_LREG) L2[s] = Lnx[s];
+                    else L2[s] = make_float2(__ldg(g.L + offs[s]), __ldg(g.L + offs[s] + 32));
+                }
+            }
+            if constexpr (METLDPC_PIPE_LREG && PC::NL == 0) {
+                if (i + 1 < nt) {
+                    const int* ix = idx + NA;
+#pragma unroll
+                    for (int s = 0; s < NA; ++s) {
+                        const uint32_t o = uint32_t(ix[s]) + uint32_t(lane);
+                        Lnx[s] = make_float2(__ldg(g.L + o), __ldg(g.L + o + 32));
+                    }
+                }
+            }
+            mbar_wait(bar_a + 8 * st, ph);
+            const float* sr = reinterpret_cast<const float*>(stage + st * PC::STG);
+#pragma unroll
+            for (int s = 0; s < NA; ++s) {
+                r2[s] = make_float2(sr[s * 64 + lane], sr[s * 64 + 32 + lane]);
+                if constexpr (PC::NL > 0)
+                    L2[s] = make_float2(sr[(NA + ND + s) * 64 + lane], sr[(NA + ND + s) * 64 + 32 + lane]);
+            }
+            float2 lam = make_float2(0.0f, 0.0f);
+            if constexpr (ND > 0) lam = make_float2(sr[NA * 64 + lane], sr[NA * 64 + 32 + lane]);
+            float* pr = g.r + (size_t(abase + jl * NA) * 64 + lane);
+            uint2 d1 = make_uint2(0, 0);
+            const uint2 c2 = cn_pair<RULE, NA, ND>(tabk, L2, r2, lam, make_uint2((swx >> lane) & 1u, (swy >> lane) & 1u),
+                                                   make_uint2((wv.x >> lane) & 1u, (wv.y >> lane) & 1u), pr, g.L, offs, d1);
+            un0 |= __ballot_sync(FULL, c2.x);
+            un1 |= __ballot_sync(FULL, c2.y);
+            if constexpr (ND > 0) {
+                const uint32_t b0 = __ballot_sync(FULL, d1.x), b1 = __ballot_sync(FULL, d1.y);
+                if (lane == 0) {
+                    uint32_t* wp = g.d1bits + (size_t(k.wpar) * cd.n_1 + dbase + jl) * 2;
+                    wp[0] = (am0 == FULL) ? b0 : ((b0 & am0) | (wp[0] & ~am0));
+                    wp[1] = (am1 == FULL) ? b1 : ((b1 & am1) | (wp[1] & ~am1));
+                }
+            }
+            __syncwarp();   // every lane has read stage st before it is refilled
         }
     }
     if (k.check && lane == 0) {
@@ -1002,6 +1276,54 @@ static void* cn_kernel(int rule, int D, int nd) {
                                       : cn_tile_kernel<METLDPC_RULE_PHI_LUT>(D, nd);
 }
 
+template <int RULE>
+static void* cn_pipe_kernel(int na, int nd) {
+    switch (na * 2 + nd) {
+        case 2: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 1, 0>);
+        case 3: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 1, 1>);
+        case 4: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 2, 0>);
+        case 5: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 2, 1>);
+        case 6: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 3, 0>);
+        case 7: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 3, 1>);
+        case 8: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 4, 0>);
+        case 9: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 4, 1>);
+    }
+    return nullptr;
+}
+
+// Pipelined kernel for classes with 1..4 active slots and <= 1 degree-1 slot (64-lane
+// groups); METLDPC_PIPE=0 selects the register-only k_cn_tile instead (A/B experiments).
+bool cn_use_pipe(int D, int nd) {
+    static const bool on = [] {
+        const char* e = std::getenv("METLDPC_PIPE");
+        return !(e && e[0] == '0');
+    }();
+    return on && D >= 0 && nd <= 1 && D - nd >= 1 && D - nd <= 4;
+}
+
+template <int NA, int ND>
+static void pipe_geom(int rule, int* threads, size_t* smem) {
+    using PC = PipeCfg<NA, ND>;
+    *threads = PC::THREADS;
+    *smem = size_t(rule == METLDPC_RULE_EXACT ? PhiT<METLDPC_RULE_EXACT>::TAB_BYTES : PhiT<METLDPC_RULE_PHI_LUT>::TAB_BYTES) +
+            size_t(PC::WARPS) * PC::WARP_BYTES;
+}
+
+static void cn_pipe_geom(int rule, int D, int nd, int* threads, size_t* smem) {
+    switch ((D - nd) * 2 + nd) {
+        case 2: pipe_geom<1, 0>(rule, threads, smem); return;
+        case 3: pipe_geom<1, 1>(rule, threads, smem); return;
+        case 4: pipe_geom<2, 0>(rule, threads, smem); return;
+        case 5: pipe_geom<2, 1>(rule, threads, smem); return;
+        case 6: pipe_geom<3, 0>(rule, threads, smem); return;
+        case 7: pipe_geom<3, 1>(rule, threads, smem); return;
+        case 8: pipe_geom<4, 0>(rule, threads, smem); return;
+        case 9: pipe_geom<4, 1>(rule, threads, smem); return;
+    }
+    *threads = 0;
+    *smem = 0;
+}
+
 int cn_tile_max(int D, int nd) { return (D - nd) <= 4 ? 32 : 8; }
 int cn_units_per_tile(int D, int nd) { return (D - nd) <= 4 ? 1 : 2; }
 
@@ -1014,6 +1336,15 @@ size_t cn_smem(int rule, int D, int nd) {
 }
 
 int cn_blocks_per_sm(int rule, int D, int nd) {
+    if (cn_use_pipe(D, nd)) {
+        void* f = rule == METLDPC_RULE_EXACT ? cn_pipe_kernel<METLDPC_RULE_EXACT>(D - nd, nd)
+                                             : cn_pipe_kernel<METLDPC_RULE_PHI_LUT>(D - nd, nd);
+        int th;
+        size_t sm;
+        cn_pipe_geom(rule, D, nd, &th, &sm);
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        return 1;
+    }
     int nb = 0;
     void* f = cn_kernel(rule, D, nd);
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cn_smem(rule, D, nd)));
@@ -1071,6 +1402,16 @@ static cudaError_t launch_with_window(void* f, dim3 grid, dim3 block, void** arg
 void launch_cn(const CodeDev& cd, const Group& g, int rule, int D, int nd, int begin, int count, int ts, int grid,
                int l, bool check, cudaStream_t s, const L2Window& w) {
     CnCtl k{check ? 1 : 0, (l - 1) & 1, l & 1, l == 0 ? 1 : 0, check ? 1 : 0};
+    if (cn_use_pipe(D, nd)) {
+        void* f = rule == METLDPC_RULE_EXACT ? cn_pipe_kernel<METLDPC_RULE_EXACT>(D - nd, nd)
+                                             : cn_pipe_kernel<METLDPC_RULE_PHI_LUT>(D - nd, nd);
+        int th;
+        size_t sm;   // the smem attribute was set by cn_blocks_per_sm
+        cn_pipe_geom(rule, D, nd, &th, &sm);
+        void* args[] = {const_cast<CodeDev*>(&cd), const_cast<Group*>(&g), &k, &begin, &count};
+        launch_with_window(f, dim3(grid), dim3(th), args, sm, s, w);
+        return;
+    }
     void* f = cn_kernel(rule, D, nd);
     if (D < 0) {
         void* args[] = {const_cast<CodeDev*>(&cd), const_cast<Group*>(&g), &k, &begin, &count};
