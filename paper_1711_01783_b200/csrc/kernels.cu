@@ -621,7 +621,7 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND>::THREADS, 1)
     using PT = PhiT<RULE>;
     using PC = PipeCfg<NA, ND>;
     constexpr int TS = 32;                     // CNs per tile
-    extern __shared__ __align__(128) char smem[];
+    extern __shared__ __align__(16) char smem[];
     __shared__ uint32_t s_unsat[2], s_act[2];
     if (*reinterpret_cast<volatile int*>(g.done)) return;
     const CnCtl k = cn_ctl(karg, g);
