@@ -3,6 +3,7 @@
 
     python tools/ncu_summary.py launches <launches.csv>      # per-kernel time and share of the step
     python tools/ncu_summary.py metrics <capture.ncu-rep>    # key roofline metrics per captured launch
+    python tools/ncu_summary.py traffic <capture.ncu-rep> N  # DRAM bytes of the CN launches per iteration
 """
 import csv
 import io
@@ -66,6 +67,32 @@ def metrics(path: str) -> str:
     return out.getvalue()
 
 
+def _bytes(v: str, unit: str) -> float:
+    return float(v.replace(",", "")) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}.get(unit, 1.0)
+
+
+def traffic(path: str, iterations: int) -> str:
+    """DRAM bytes (read + write) of the captured CN launches per iteration, as the JSON
+    bench.py reads for roofline.traffic (profiles/cn_traffic.json)."""
+    import json
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    ir, iw = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+    ik = hdr.index("Kernel Name")
+    tot, kernels = 0.0, []
+    for r in rows[2:]:
+        b = _bytes(r[ir], units[ir]) + _bytes(r[iw], units[iw])
+        tot += b
+        kernels.append({"kernel": _short(r[ik]), "dram_bytes": b})
+    return json.dumps({"source": path, "iterations": iterations, "dram_bytes_per_launch": tot / iterations,
+                       "note": "sum over the CN-phase launches of one iteration (all degree classes), one 64-lane group",
+                       "launches": kernels}, indent=1) + "\n"
+
+
 if __name__ == "__main__":
     mode, path = sys.argv[1], sys.argv[2]
-    sys.stdout.write(launches(path) if mode == "launches" else metrics(path))
+    if mode == "traffic":
+        sys.stdout.write(traffic(path, int(sys.argv[3]) if len(sys.argv) > 3 else 1))
+    else:
+        sys.stdout.write(launches(path) if mode == "launches" else metrics(path))
