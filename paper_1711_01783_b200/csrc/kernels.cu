@@ -322,34 +322,16 @@ __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 
     return make_uint2(chk0, chk1);
 }
 
-// Asynchronous L2 prefetch of a contiguous range by the TMA unit (no registers held).
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
-// One-line L2 prefetch (no registers held; the line is fetched by L2 while the warp computes).
-__device__ __forceinline__ void prefetch_line_l2(const void* p) {
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
-#ifndef METLDPC_CN_PFL
-#define METLDPC_CN_PFL 0    // CNs of look-ahead for per-lane r / lambda line prefetches into L2
-#endif
-
 #ifndef METLDPC_CN_PAIR
 #define METLDPC_CN_PAIR 1   // two-lane path with packed fp32x2 ops (FADD2 / FFMA2)
 #endif
-#ifndef METLDPC_CN_PF
-#define METLDPC_CN_PF 0     // CNs of look-ahead for an r / lambda L2 prefetch (0: off; measured
-#endif                      // slower at 4 and 8 -- the kernel is issue-bound, not DRAM-latency-bound)
 
 // One degree class (CN labels [begin, begin + count), NA active + ND <= 1 degree-1 slots)
 // for 64-lane groups.  Work unit = a tile of ts consecutive CNs owned by one warp; for
 // NA <= 4 the warp covers both 32-lane chunks (each thread: lanes `lane` and `lane + 32`,
 // two independent dependency chains), for larger NA one chunk per unit (register budget).
-// The tile's metadata is one coalesced load per array, its active-edge VN indices
-// (pre-scaled to row offsets) are staged in shared memory, and the r / lambda rows of
-// the CN PF positions ahead are prefetched into L2 by the TMA unit.
+// The tile's metadata is one coalesced load per array and its active-edge VN indices
+// (pre-scaled to row offsets) are staged in shared memory.
 template <int NA>
 __host__ __device__ constexpr int cn_tile_min_blocks() { return NA <= 4 ? 2 : 1; }   // NA > 4: 128 registers
 
@@ -399,52 +381,10 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
                 for (int e = lane; e < nt * NA; e += 32) s_idx[e] = __ldg(cd.a_vn + A0 + e) * 128;
                 __syncwarp();
             }
-            if (METLDPC_CN_PF > 0 && lane < min(nt, METLDPC_CN_PF)) {   // look-ahead for the first CNs
-                if constexpr (NA > 0) prefetch_l2(g.r + size_t(a_l) * 64, NA * 256);
-                if constexpr (ND > 0) prefetch_l2(g.lam1 + size_t(d_l) * 64, 256);
-            }
-            // Exact-degree classes: CN i of the tile owns r rows A0 + i NA .. + NA and lambda row
-            // Q0 + i, so its 128-byte lines are known without metadata.  Lane k prefetches line
-            // k mod LPC of CN (k / LPC) of a round of CPR CNs, PFL CNs ahead of the compute.
-            constexpr int PFL = (LPT == 2 && NA > 0) ? METLDPC_CN_PFL : 0;
-            constexpr int LPC = 2 * NA + 2 * ND, CPR = (LPC > 0 && LPC <= 32) ? 32 / LPC : 1;
-            const char* pf_base = nullptr;
-            size_t pf_step = 0;
-            int pf_cn = 0;
-            bool pf_ok = false;
-            if constexpr (PFL > 0) {
-                const int Q0 = __shfl_sync(FULL, d_l, 0);
-                pf_cn = lane / LPC;
-                const int line = lane % LPC;
-                pf_ok = lane < CPR * LPC;
-                if (line < 2 * NA) {
-                    pf_base = reinterpret_cast<const char*>(g.r + size_t(A0 + pf_cn * NA) * 64) + line * 128;
-                    pf_step = size_t(NA) * 256;
-                } else {
-                    pf_base = reinterpret_cast<const char*>(g.lam1 + size_t(Q0 + pf_cn) * 64) + (line - 2 * NA) * 128;
-                    pf_step = 256;
-                }
-                for (int c = 0; c < PFL; c += CPR)
-                    if (pf_ok && c + pf_cn < nt) prefetch_line_l2(pf_base + size_t(c) * pf_step);
-            }
             for (int i = 0; i < nt; ++i) {
-                if constexpr (PFL > 0) {
-                    if (i % CPR == 0) {
-                        const int c = i + PFL;
-                        if (pf_ok && c + pf_cn < nt) prefetch_line_l2(pf_base + size_t(c) * pf_step);
-                    }
-                }
                 const int ab = __shfl_sync(FULL, a_l, i);
                 const int q0 = __shfl_sync(FULL, d_l, i);
                 const uint32_t swx = __shfl_sync(FULL, sw_l.x, i), swy = __shfl_sync(FULL, sw_l.y, i);
-                if (METLDPC_CN_PF > 0) {
-                    const int ip = i + METLDPC_CN_PF;    // keep the DRAM stream PF CNs ahead
-                    const int abp = __shfl_sync(FULL, a_l, ip & 31), q0p = __shfl_sync(FULL, d_l, ip & 31);
-                    if (lane == 0 && ip < nt) {
-                        if constexpr (NA > 0) prefetch_l2(g.r + size_t(abp) * 64, NA * 256);
-                        if constexpr (ND > 0) prefetch_l2(g.lam1 + size_t(q0p) * 64, 256);
-                    }
-                }
                 const int* idx = s_idx + (ab - A0);
                 const uint32_t lo = uint32_t(c0 * 32 + lane);
                 float* pL = g.L + lo;
@@ -458,29 +398,15 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
                     if constexpr (NA <= 4) offs[s] = uint32_t(o) + lo;
 #pragma unroll
                     for (int h = 0; h < LPT; ++h) {
-#if defined(METLDPC_EXP_L_LOCAL)   // timing experiment only: L gathers from one row (L1 hits)
-                        Lv[h][s] = __ldg(g.L + lo + s * 4 + h * 32);
-#else
                         Lv[h][s] = (NA <= 4) ? __ldg(g.L + offs[s] + h * 32) : __ldg(pL + o + h * 32);
-#endif
-#if defined(METLDPC_EXP_NO_R)      // timing experiment only: no r reads
-                        ro[h][s] = __uint_as_float(lo * 7u + uint32_t(s));
-#else
                         ro[h][s] = __ldcs(pr + s * 64 + h * 32);   // r^0 = 0: zeroed at group begin
-#endif
                     }
                 }
                 uint2 wv = make_uint2(0, 0);
                 if constexpr (ND > 0) {
                     const float* pl = g.lam1 + (size_t(q0) * 64 + c0 * 32 + lane);
 #pragma unroll
-                    for (int h = 0; h < LPT; ++h) {
-#if defined(METLDPC_EXP_NO_R)
-                        lam[h] = __uint_as_float(lo * 5u + uint32_t(h) + uint32_t(q0));
-#else
-                        lam[h] = __ldcs(pl + h * 32);
-#endif
-                    }
+                    for (int h = 0; h < LPT; ++h) lam[h] = __ldcs(pl + h * 32);
                     if (k.check) wv = __ldg(reinterpret_cast<const uint2*>(g.d1bits) + (size_t(k.rpar) * cd.n_1 + q0));
                 } else {
 #pragma unroll
