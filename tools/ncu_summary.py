@@ -4,6 +4,7 @@
     python tools/ncu_summary.py launches <launches.csv>      # per-kernel time and share of the step
     python tools/ncu_summary.py metrics <capture.ncu-rep>    # key roofline metrics per captured launch
     python tools/ncu_summary.py traffic <capture.ncu-rep> N  # DRAM bytes of the CN launches per iteration
+    python tools/ncu_summary.py stalls <capture.ncu-rep>     # stall reasons + hottest SASS lines
 """
 import csv
 import io
@@ -90,9 +91,56 @@ def traffic(path: str, iterations: int) -> str:
                        "launches": kernels}, indent=1) + "\n"
 
 
+def stalls(path: str, top: int = 12) -> str:
+    """Warp-stall reasons per issued instruction and the hottest SASS lines of each captured kernel."""
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr = rows[0]
+    out = io.StringIO()
+    for r in rows[2:]:
+        out.write(_short(r[hdr.index("Kernel Name")]) + "  (warps stalled per issued instruction)\n")
+        st = []
+        for i, h in enumerate(hdr):
+            m = re.match(r"smsp__average_warps_issue_stalled_(\w+)_per_issue_active\.ratio", h)
+            if m:
+                try:
+                    st.append((float(r[i]), m.group(1)))
+                except ValueError:
+                    pass
+        for v, name in sorted(st, reverse=True)[:8]:
+            out.write(f"    {name:28s} {v:8.3f}\n")
+    src = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(src)))
+    i = 0
+    while i < len(rows):
+        if rows[i] and rows[i][0] == "Kernel Name":
+            name = _short(rows[i][1])
+            hdr = rows[i + 1]
+            body = []
+            i += 2
+            while i < len(rows) and len(rows[i]) == len(hdr):
+                body.append(dict(zip(hdr, rows[i])))
+                i += 1
+            def f(x):
+                try:
+                    return float(x)
+                except ValueError:
+                    return 0.0
+            tot = sum(f(d["Warp Stall Sampling (All Samples)"]) for d in body) or 1.0
+            out.write(f"{name}: hottest SASS lines (share of stall samples)\n")
+            for d in sorted(body, key=lambda d: -f(d["Warp Stall Sampling (All Samples)"]))[:top]:
+                out.write(f"    {100 * f(d['Warp Stall Sampling (All Samples)']) / tot:5.1f}%  {d['Source'].strip()[:70]}\n")
+        else:
+            i += 1
+    return out.getvalue()
+
+
 if __name__ == "__main__":
     mode, path = sys.argv[1], sys.argv[2]
-    if mode == "traffic":
+    if mode == "stalls":
+        sys.stdout.write(stalls(path))
+    elif mode == "traffic":
         sys.stdout.write(traffic(path, int(sys.argv[3]) if len(sys.argv) > 3 else 1))
     else:
         sys.stdout.write(launches(path) if mode == "launches" else metrics(path))
