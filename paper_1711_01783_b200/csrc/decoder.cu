@@ -675,6 +675,25 @@ metldpc_status metldpc_decode(metldpc_decoder d, int32_t batch, const float* llr
     const HostLayout& L = d->code->host;
     const size_t W = size_t(L.m + 31) / 32, NW = size_t(L.n + 31) / 32;
     const int groups = (batch + d->B - 1) / d->B;
+    if (d->K > 1 && d->use_graph && !d->profiling && groups > d->K) {
+        // Group queue: workspace k decodes groups k, k + K, ... on its own stream with no
+        // per-round join, so with early termination a workspace whose group finished early
+        // starts its next group at once instead of waiting for the round's slowest group.
+        CUDA_TRY(cudaEventRecord(d->fork_ev[0], s));
+        for (int k = 0; k < d->K; ++k) CUDA_TRY(cudaStreamWaitEvent(d->gs[size_t(k)], d->fork_ev[0], 0));
+        for (int gi = 0; gi < groups; ++gi) {
+            const int k = gi % d->K, f0 = gi * d->B;
+            GroupJob j{k, llr + size_t(f0) * L.n, syndrome + size_t(f0) * W, std::min(d->B, batch - f0),
+                       bits_out + size_t(f0) * NW, iters_out + f0, conv_out + f0, d->gs[size_t(k)]};
+            metldpc_status st;
+            if ((st = group_begin(d, j, N)) || (st = group_loop(d, j, N)) || (st = group_end(d, j, N))) return st;
+        }
+        for (int k = 0; k < d->K; ++k) {
+            CUDA_TRY(cudaEventRecord(d->join_ev[size_t(k)], d->gs[size_t(k)]));
+            CUDA_TRY(cudaStreamWaitEvent(s, d->join_ev[size_t(k)], 0));
+        }
+        return METLDPC_OK;
+    }
     for (int g0 = 0; g0 < groups; g0 += d->K) {
         std::vector<GroupJob> jobs;
         for (int k = 0; k < d->K && g0 + k < groups; ++k) {
@@ -733,7 +752,44 @@ metldpc_status host_pipeline(metldpc_decoder d, int32_t batch, int md, int32_t d
     }
     const int groups = (batch + d->B - 1) / d->B;
     st = METLDPC_OK;
-    for (int g0 = 0, round = 0; g0 < groups && st == METLDPC_OK; g0 += K, ++round) {
+    const bool queue = K > 1 && d->use_graph && !d->profiling;
+    // Group queue (as in metldpc_decode): group gi uses staging slot gi mod 2K and workspace
+    // gi mod K on that workspace's stream, ordered only by its own events (inputs staged,
+    // previous occupant of the slot decoded and copied out) -- no per-round join.
+    for (int gi = 0; queue && gi < groups && st == METLDPC_OK; ++gi) {
+        const int k = gi % K, slot = gi % S;
+        auto& sl = d->st[size_t(slot)];
+        const int f0 = gi * d->B, nb = std::min(d->B, batch - f0);
+        cudaStream_t gs = d->gs[size_t(k)];
+        cudaStreamWaitEvent(d->s_h2d, slot_free[size_t(slot)], 0);
+        cudaStreamWaitEvent(d->s_h2d, out_free[size_t(slot)], 0);
+        cudaMemcpyAsync(sl.llr, in_h + size_t(f0) * n, size_t(nb) * n * sizeof(float), cudaMemcpyHostToDevice, d->s_h2d);
+        if (md && xnorm_h)
+            cudaMemcpyAsync(sl.xnorm, xnorm_h + size_t(f0) * nx, size_t(nb) * nx * sizeof(float), cudaMemcpyHostToDevice,
+                            d->s_h2d);
+        cudaMemcpyAsync(sl.synd, synd_h + size_t(f0) * W, size_t(nb) * W * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                        d->s_h2d);
+        if (md) {
+            launch_md_llr(int64_t(nb) * int64_t(n), int(n), dim, c_md, sl.llr, xnorm_h ? sl.xnorm : nullptr, sl.llr,
+                          d->s_h2d);
+            d->prof.launches++;
+        }
+        cudaEventRecord(in_ready[size_t(slot)], d->s_h2d);
+        cudaStreamWaitEvent(gs, in_ready[size_t(slot)], 0);
+        GroupJob j{k, sl.llr, sl.synd, nb, sl.bits, sl.iters, sl.conv, gs};
+        if ((st = group_begin(d, j, N)) || (st = group_loop(d, j, N)) || (st = group_end(d, j, N))) break;
+        cudaEventRecord(out_ready[size_t(slot)], gs);
+        cudaEventRecord(slot_free[size_t(slot)], gs);
+        cudaStreamWaitEvent(d->s_d2h, out_ready[size_t(slot)], 0);
+        cudaMemcpyAsync(bits_h + size_t(f0) * NW, sl.bits, size_t(nb) * NW * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                        d->s_d2h);
+        cudaMemcpyAsync(iters_h + f0, sl.iters, size_t(nb) * sizeof(int32_t), cudaMemcpyDeviceToHost, d->s_d2h);
+        cudaMemcpyAsync(conv_h + f0, sl.conv, size_t(nb), cudaMemcpyDeviceToHost, d->s_d2h);
+        cudaEventRecord(out_free[size_t(slot)], d->s_d2h);
+    }
+    if (queue)
+        for (int k = 0; k < K; ++k) cudaStreamSynchronize(d->gs[size_t(k)]);
+    for (int g0 = 0, round = 0; !queue && g0 < groups && st == METLDPC_OK; g0 += K, ++round) {
         std::vector<GroupJob> jobs;
         std::vector<int> slots;
         for (int k = 0; k < K && g0 + k < groups; ++k) {

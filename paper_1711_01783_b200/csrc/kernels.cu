@@ -488,6 +488,9 @@ constexpr int kSmemPerSm = 232448;     // opt-in dynamic shared memory per block
 #ifndef METLDPC_PIPE_L
 #define METLDPC_PIPE_L 0   // 1: the L rows also come by TMA (measured slower: 0.59 vs 0.54 ms at C3)
 #endif
+#ifndef METLDPC_PIPE_LPF
+#define METLDPC_PIPE_LPF 0    // CNs of look-ahead for an L1 prefetch of the L lines (0: off)
+#endif
 #ifndef METLDPC_PIPE_LREG
 #define METLDPC_PIPE_LREG 0   // 1: the next CN's L gathers are issued into registers one CN ahead
 #endif
@@ -625,6 +628,15 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND>::THREADS, 1)
         }
         for (int i = 0; i < nt; ++i) {
             produce();
+            if constexpr (METLDPC_PIPE_LPF > 0 && PC::NL == 0) {
+                // L1 prefetch of the L lines (2 per active slot) of CN i + LPF: lane 2s + h
+                // takes chunk h of slot s; no registers held, the gathers of that CN then hit L1.
+                const int ip = i + METLDPC_PIPE_LPF;
+                if (ip < nt && lane < 2 * NA) {
+                    const float* a = g.L + s_idx[cb * PC::IDX + ip * NA + (lane >> 1)] + (lane & 1) * 32;
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+                }
+            }
             const uint32_t st = nc % kPipeStages, ph = (nc / kPipeStages) & 1u;
             ++nc;
             const uint32_t swx = __shfl_sync(FULL, sw_l.x, i), swy = __shfl_sync(FULL, sw_l.y, i);
