@@ -65,6 +65,7 @@ def parse():
     ap.add_argument("--distinct", type=int, default=64, help="distinct frames generated per rank (tiled)")
     ap.add_argument("--rule", choices=["exact", "lut"], default="exact")
     ap.add_argument("--no-et", action="store_true")
+    ap.add_argument("--refill", action="store_true", help="lane refill (streaming decode, metldpc_config_t.lane_refill)")
     ap.add_argument("--no-skip", action="store_true",
                     help="iterate degree-1 VNs too (Table 1 'without skipping', METLDPC_CODE_NO_SKIP)")
     ap.add_argument("--lanes", type=int, default=64)
@@ -258,7 +259,7 @@ def main():
     hc = B.Code(code, device=local, no_skip=a.no_skip)
     st = dict(st, iter_edges=hc.info.iter_edges, n_deg1=hc.info.n_deg1, n_active=hc.info.n_active)
     dec = B.Decoder(hc, F, rule=_rule(a), max_iter=a.iters, early_term=not a.no_et, lanes_per_group=a.lanes,
-                    groups_in_flight=a.groups)
+                    groups_in_flight=a.groups, lane_refill=a.refill)
     llr = torch.empty_like(v)
     nw = (a.n + 31) // 32
     bits = torch.empty((F, nw), dtype=torch.int32, device=dev)

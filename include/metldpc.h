@@ -63,6 +63,11 @@ typedef struct {
     int32_t groups_in_flight;  /* lane groups decoded concurrently on their own streams, 1..8;
                                   default 4 (each has its own ~1 GB workspace at C3; their
                                   kernels fill each other's ramps, tails and launch gaps)   */
+    int32_t lane_refill;       /* 1 = streaming decode (needs early_term, 64-lane groups): a lane
+                                  whose frame has latched takes the next frame of the batch in
+                                  a refill wave while the other lanes keep iterating, so a
+                                  group no longer waits for its slowest frame; per-frame
+                                  results are identical to group mode.  Default 0.           */
 } metldpc_config_t;
 
 typedef struct {

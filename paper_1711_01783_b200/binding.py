@@ -34,7 +34,7 @@ class MetLdpcError(RuntimeError):
 
 class Config(C.Structure):
     _fields_ = [("rule", C.c_int32), ("max_iter", C.c_int32), ("early_term", C.c_int32),
-                ("lanes_per_group", C.c_int32), ("groups_in_flight", C.c_int32)]
+                ("lanes_per_group", C.c_int32), ("groups_in_flight", C.c_int32), ("lane_refill", C.c_int32)]
 
 
 class CodeInfo(C.Structure):
@@ -281,11 +281,13 @@ class Decoder:
     """Decoder workspace; ``decode`` takes torch CUDA tensors and returns torch tensors."""
 
     def __init__(self, code: Code, max_batch: int, rule: int = RULE_EXACT, max_iter: int = 100,
-                 early_term: bool = True, lanes_per_group: int = 64, groups_in_flight: int | None = None):
+                 early_term: bool = True, lanes_per_group: int = 64, groups_in_flight: int | None = None,
+                 lane_refill: bool = False):
         cfg = metldpc_config_default()
         cfg.rule, cfg.max_iter, cfg.early_term, cfg.lanes_per_group = rule, max_iter, int(early_term), lanes_per_group
         if groups_in_flight is not None:
             cfg.groups_in_flight = groups_in_flight
+        cfg.lane_refill = int(lane_refill)
         self.cfg = cfg
         self.code = code
         self.max_batch = max_batch

@@ -48,6 +48,8 @@ struct metldpc_decoder_s {
     struct Workspace {
         float *r = nullptr, *L = nullptr, *lam_a = nullptr, *lam1 = nullptr;
         uint32_t *d1bits = nullptr, *synd_t = nullptr, *ctl = nullptr;  // ctl: act[4] unsat[4] invalid[4]
+                                                                          // iter maxit . . fresh[4] fin[4] newm[4]
+        int32_t *lane_l = nullptr, *lane_frame = nullptr, *lane_fbuf = nullptr;   // lane refill
         int32_t* iters = nullptr;
         uint8_t* conv = nullptr;
         int32_t* done = nullptr;
@@ -58,6 +60,8 @@ struct metldpc_decoder_s {
     // CUDA-graph iteration loop per workspace: a conditional WHILE node whose
     // body is CN classes -> latch -> finish -> loop control; built on first use.
     std::vector<cudaGraphExec_t> loop_exec;
+    std::vector<cudaGraphExec_t> stream_exec;       // lane-refill graph per workspace
+    StreamJob* job = nullptr;                       // frame queue of a streaming decode (device)
     int use_graph = 1;
     std::vector<cudaStream_t> gs;                   // one stream per workspace (K > 1)
     std::vector<cudaEvent_t> fork_ev, join_ev;
@@ -140,6 +144,12 @@ Group group_of(metldpc_decoder d, int k) {
     g.done = w.done;
     g.iter = reinterpret_cast<int32_t*>(w.ctl + 12);
     g.maxit = reinterpret_cast<int32_t*>(w.ctl + 13);
+    g.fresh = w.ctl + 16;
+    g.fin = w.ctl + 20;
+    g.newm = w.ctl + 24;
+    g.lane_l = w.lane_l;
+    g.lane_frame = w.lane_frame;
+    g.lane_fbuf = w.lane_fbuf;
     return g;
 }
 
@@ -338,6 +348,137 @@ metldpc_status group_loop(metldpc_decoder d, const GroupJob& j, int N) {
     return METLDPC_OK;
 }
 
+// Lane-refill graph of workspace k ("refill ... from a frame queue", per lane):
+//   while (some lane iterates or waits) {
+//       CN classes; latch (per lane); finish;
+//       if (wave) { finalize finished lanes; assign next frames; scatter; syndrome; activate }
+//       pass counter++ }
+// The refill wave is an IF node, so passes without a wave cost nothing extra.
+metldpc_status stream_graph(metldpc_decoder d, int k, cudaGraphExec_t* out) {
+    if (d->stream_exec[size_t(k)]) {
+        *out = d->stream_exec[size_t(k)];
+        return METLDPC_OK;
+    }
+    const CodeDev cd = code_dev(d->code, d->cfg.rule);
+    const Group g = group_of(d, k);
+    cudaGraph_t graph;
+    CUDA_TRY(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle hw;
+    CUDA_TRY(cudaGraphConditionalHandleCreate(&hw, graph, 1u, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams wp{};
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = hw;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    CUDA_TRY(cudaGraphAddNode(&wnode, graph, nullptr, 0, &wp));
+    cudaGraph_t body = wp.conditional.phGraph_out[0];
+    cudaGraphConditionalHandle hi;
+    CUDA_TRY(cudaGraphConditionalHandleCreate(&hi, body, 0u, cudaGraphCondAssignDefault));
+    cudaStream_t cs;
+    CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    auto fail_capture = [&](cudaError_t e, const char* what) {
+        cudaStreamDestroy(cs);
+        cudaGraphDestroy(graph);
+        return fail(METLDPC_ECUDA, std::string(what) + cudaGetErrorString(e));
+    };
+    // part A: one pass (CN classes, per-lane latch, finish)
+    cudaError_t e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
+    if (e != cudaSuccess) return fail_capture(e, "stream graph capture: ");
+    for (const auto& c : d->cn_classes)
+        launch_cn(cd, g, d->cfg.rule, c.D, c.nd, c.begin, c.count, c.ts, c.grid, 0, true, cs, d->l2w[size_t(k)]);
+    launch_latch_stream(g, d->job, (unsigned long long)hi, cs);
+    launch_finish(cd, g, d->vn_grid, cs, d->l2w[size_t(k)]);
+    cudaGraph_t cap;
+    if ((e = cudaStreamEndCapture(cs, &cap)) != cudaSuccess) return fail_capture(e, "stream graph capture: ");
+    // the last node of part A (a single-stream capture is a chain: the node without successors)
+    size_t nn = 0;
+    cudaGraphGetNodes(body, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    cudaGraphGetNodes(body, nodes.data(), &nn);
+    cudaGraphNode_t last = nullptr;
+    for (auto nd : nodes) {
+        size_t nout = 0;
+        cudaGraphNodeGetDependentNodes(nd, nullptr, &nout);
+        if (nout == 0) last = nd;
+    }
+    // IF node: the refill wave
+    cudaGraphNodeParams ip{};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = hi;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    cudaGraphNode_t inode;
+    if ((e = cudaGraphAddNode(&inode, body, &last, 1, &ip)) != cudaSuccess) return fail_capture(e, "stream graph IF: ");
+    cudaGraph_t wave = ip.conditional.phGraph_out[0];
+    if ((e = cudaStreamBeginCaptureToGraph(cs, wave, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)) != cudaSuccess)
+        return fail_capture(e, "stream graph capture: ");
+    launch_refill_wave(cd, g, d->job, cs);
+    if ((e = cudaStreamEndCapture(cs, &cap)) != cudaSuccess) return fail_capture(e, "stream graph capture: ");
+    // part C: pass counter and loop condition, after the IF node
+    if ((e = cudaStreamBeginCaptureToGraph(cs, body, &inode, nullptr, 1, cudaStreamCaptureModeRelaxed)) != cudaSuccess)
+        return fail_capture(e, "stream graph capture: ");
+    launch_stream_ctl(g, (unsigned long long)hw, cs);
+    if ((e = cudaStreamEndCapture(cs, &cap)) != cudaSuccess) return fail_capture(e, "stream graph capture: ");
+    cudaStreamDestroy(cs);
+    cudaGraphExec_t exec;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return fail(METLDPC_ECUDA, std::string("stream graph instantiate: ") + cudaGetErrorString(e));
+    d->stream_exec[size_t(k)] = exec;
+    *out = exec;
+    return METLDPC_OK;
+}
+
+bool stream_mode(metldpc_decoder d) {
+    return d->cfg.lane_refill && d->job && d->cfg.early_term && d->use_graph && !d->profiling && d->B == 64;
+}
+
+// Streaming decode of a whole batch: every workspace runs its refill graph on its own stream,
+// all drawing frames from one device-side queue (StreamJob::next).
+metldpc_status stream_decode(metldpc_decoder d, int32_t batch, const float* llr, const uint32_t* synd, int N,
+                             uint32_t* bits_out, int32_t* iters_out, uint8_t* conv_out, cudaStream_t s) {
+    const CodeDev cd = code_dev(d->code, d->cfg.rule);
+    StreamJob h{};
+    h.llr = llr;
+    h.synd = synd;
+    h.bits = bits_out;
+    h.iters = iters_out;
+    h.conv = conv_out;
+    h.nframes = batch;
+    h.next = 0;
+    h.N = N;
+    {
+        const char* e = std::getenv("METLDPC_REFILL_MIN");
+        h.wave_min = (e && std::atoi(e) > 0) ? std::atoi(e) : 16;
+    }
+    CUDA_TRY(cudaMemcpyAsync(d->job, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+    const int K = std::min(d->K, (batch + d->B - 1) / d->B);
+    if (K > 1) {
+        CUDA_TRY(cudaEventRecord(d->fork_ev[0], s));
+        for (int k = 0; k < K; ++k) CUDA_TRY(cudaStreamWaitEvent(d->gs[size_t(k)], d->fork_ev[0], 0));
+    }
+    for (int k = 0; k < K; ++k) {
+        cudaStream_t ks = K > 1 ? d->gs[size_t(k)] : s;
+        const Group g = group_of(d, k);
+        cudaGraphExec_t exec;
+        metldpc_status st = stream_graph(d, k, &exec);
+        if (st) return st;
+        launch_stream_init(g, ks);
+        launch_refill_wave(cd, g, d->job, ks);   // first fill
+        CUDA_TRY(cudaGraphLaunch(exec, ks));
+        d->prof.launches += 6;
+        d->last_ws = k;
+    }
+    if (K > 1)
+        for (int k = 0; k < K; ++k) {
+            CUDA_TRY(cudaEventRecord(d->join_ev[size_t(k)], d->gs[size_t(k)]));
+            CUDA_TRY(cudaStreamWaitEvent(s, d->join_ev[size_t(k)], 0));
+        }
+    CUDA_TRY(cudaGetLastError());
+    return METLDPC_OK;
+}
+
 // Decodes up to K groups concurrently: forked from stream `s` onto the workspace streams,
 // iterations interleaved group by group, joined back into `s`.
 metldpc_status decode_round(metldpc_decoder d, std::vector<GroupJob>& jobs, int N, cudaStream_t s) {
@@ -496,13 +637,14 @@ metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, cons
         if ((s = dalloc(&w.r, size_t(L.E_it) * B)) || (s = dalloc(&w.L, 2 * size_t(L.n_a) * B)) ||
             (s = dalloc(&w.lam_a, size_t(L.n_a) * B)) || (s = dalloc(&w.lam1, size_t(L.n_1) * B)) ||
             (s = dalloc(&w.d1bits, 2 * size_t(L.n_1) * C)) || (s = dalloc(&w.synd_t, size_t(L.m) * C)) ||
-            (s = dalloc(&w.ctl, 16)) || (s = dalloc(&w.iters, B)) || (s = dalloc(&w.conv, B)) ||
+            (s = dalloc(&w.ctl, 32)) || (s = dalloc(&w.iters, B)) || (s = dalloc(&w.conv, B)) ||
+            (s = dalloc(&w.lane_l, B)) || (s = dalloc(&w.lane_frame, B)) || (s = dalloc(&w.lane_fbuf, B)) ||
             (s = dalloc(&w.done, 1))) {
             metldpc_decoder_destroy(d);
             return s;
         }
         cudaMemset(w.d1bits, 0, 2 * size_t(L.n_1) * C * sizeof(uint32_t));
-        cudaMemset(w.ctl, 0, 16 * sizeof(uint32_t));
+        cudaMemset(w.ctl, 0, 32 * sizeof(uint32_t));
     }
     // Persisting-L2 window over the workspace's L / accumulator rows (the CN gathers and
     // atomics hit them ~23 times per iteration per VN).  Measured (round 1, C3): +2 % with one
@@ -529,6 +671,14 @@ metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, cons
         cudaGetLastError();
     }
     d->loop_exec.assign(size_t(d->K), nullptr);
+    d->stream_exec.assign(size_t(d->K), nullptr);
+    if (cfg.lane_refill) {
+        if (cudaMalloc(reinterpret_cast<void**>(&d->job), sizeof(StreamJob)) != cudaSuccess) {
+            cudaGetLastError();
+            metldpc_decoder_destroy(d);
+            return fail(METLDPC_ENOMEM, "device allocation (stream job)");
+        }
+    }
     {
         const char* e = std::getenv("METLDPC_GRAPH");
         d->use_graph = (e && *e == '0') ? 0 : 1;
@@ -576,12 +726,18 @@ void metldpc_decoder_destroy(metldpc_decoder d) {
         dfree(w.d1bits);
         dfree(w.synd_t);
         dfree(w.ctl);
+        dfree(w.lane_l);
+        dfree(w.lane_frame);
+        dfree(w.lane_fbuf);
         dfree(w.iters);
         dfree(w.conv);
         dfree(w.done);
     }
     for (auto ex : d->loop_exec)
         if (ex) cudaGraphExecDestroy(ex);
+    for (auto ex : d->stream_exec)
+        if (ex) cudaGraphExecDestroy(ex);
+    if (d->job) cudaFree(d->job);
     for (auto st : d->gs) cudaStreamDestroy(st);
     for (auto e : d->join_ev) cudaEventDestroy(e);
     for (auto e : d->fork_ev) cudaEventDestroy(e);
@@ -675,6 +831,7 @@ metldpc_status metldpc_decode(metldpc_decoder d, int32_t batch, const float* llr
     const HostLayout& L = d->code->host;
     const size_t W = size_t(L.m + 31) / 32, NW = size_t(L.n + 31) / 32;
     const int groups = (batch + d->B - 1) / d->B;
+    if (stream_mode(d)) return stream_decode(d, batch, llr, syndrome, N, bits_out, iters_out, conv_out, s);
     if (d->K > 1 && d->use_graph && !d->profiling && groups > d->K) {
         // Group queue: workspace k decodes groups k, k + K, ... on its own stream with no
         // per-round join, so with early termination a workspace whose group finished early

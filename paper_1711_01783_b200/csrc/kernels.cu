@@ -344,11 +344,15 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
     constexpr int NAS = NA > 0 ? NA : 1;
     constexpr int STAGE = (NA <= 4 ? 32 : 8) * NAS;
     extern __shared__ __align__(16) char smem[];
-    __shared__ uint32_t s_unsat[2], s_act[2];
+    __shared__ uint32_t s_unsat[2], s_act[2], s_fresh[2];
     if (*reinterpret_cast<volatile int*>(g.done)) return;
     const CnCtl k = cn_ctl(karg, g);
     load_phi_table<RULE>(smem, cd.phi);
-    if (threadIdx.x < 2) { s_unsat[threadIdx.x] = 0u; s_act[threadIdx.x] = g.act[threadIdx.x]; }
+    if (threadIdx.x < 2) {
+        s_unsat[threadIdx.x] = 0u;
+        s_act[threadIdx.x] = g.act[threadIdx.x];
+        s_fresh[threadIdx.x] = g.fresh[threadIdx.x];
+    }
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t tabk = phi_tab_lane<RULE>(smem, lane);
@@ -401,6 +405,13 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
                         Lv[h][s] = (NA <= 4) ? __ldg(g.L + offs[s] + h * 32) : __ldg(pL + o + h * 32);
                         ro[h][s] = __ldcs(pr + s * 64 + h * 32);   // r^0 = 0: zeroed at group begin
                     }
+                }
+                if (s_fresh[0] | s_fresh[1]) {   // lane refill: r^0 = 0 for a frame starting in this pass
+#pragma unroll
+                    for (int h = 0; h < LPT; ++h)
+                        if ((s_fresh[c0 + h] >> lane) & 1u)
+#pragma unroll
+                            for (int s = 0; s < NA; ++s) ro[h][s] = 0.0f;
                 }
                 uint2 wv = make_uint2(0, 0);
                 if constexpr (ND > 0) {
@@ -551,11 +562,15 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND>::THREADS, 1)
     using PC = PipeCfg<NA, ND>;
     constexpr int TS = 32;                     // CNs per tile
     extern __shared__ __align__(16) char smem[];
-    __shared__ uint32_t s_unsat[2], s_act[2];
+    __shared__ uint32_t s_unsat[2], s_act[2], s_fresh[2];
     if (*reinterpret_cast<volatile int*>(g.done)) return;
     const CnCtl k = cn_ctl(karg, g);
     load_phi_table<RULE>(smem, cd.phi);
-    if (threadIdx.x < 2) { s_unsat[threadIdx.x] = 0u; s_act[threadIdx.x] = g.act[threadIdx.x]; }
+    if (threadIdx.x < 2) {
+        s_unsat[threadIdx.x] = 0u;
+        s_act[threadIdx.x] = g.act[threadIdx.x];
+        s_fresh[threadIdx.x] = g.fresh[threadIdx.x];
+    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     char* wb = smem + PT::TAB_BYTES + warp * PC::WARP_BYTES;
     int* s_idx = reinterpret_cast<int*>(wb);                         // [2][IDX]
@@ -569,6 +584,7 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND>::THREADS, 1)
     __syncthreads();
     const uint32_t tabk = phi_tab_lane<RULE>(smem, lane);
     const uint32_t am0 = s_act[0], am1 = s_act[1];
+    const bool any_fresh = (s_fresh[0] | s_fresh[1]) != 0u;   // lane refill: frames starting now
     const int abase = __ldg(cd.cn_aptr + begin);
     const int dbase = ND ? __ldg(cd.cn_dptr + begin) : 0;
     const int ntiles = (count + TS - 1) / TS;
@@ -669,6 +685,14 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND>::THREADS, 1)
             }
             mbar_wait(bar_a + 8 * st, ph);
             const float* sr = reinterpret_cast<const float*>(stage + st * PC::STG);
+            if (any_fresh) {   // r^0 = 0 for a lane whose frame starts in this pass (Step 2)
+                const bool f0 = (s_fresh[0] >> lane) & 1u, f1 = (s_fresh[1] >> lane) & 1u;
+#pragma unroll
+                for (int s = 0; s < NA; ++s) {
+                    if (f0) reinterpret_cast<float*>(stage + st * PC::STG)[s * 64 + lane] = 0.0f;
+                    if (f1) reinterpret_cast<float*>(stage + st * PC::STG)[s * 64 + 32 + lane] = 0.0f;
+                }
+            }
 #pragma unroll
             for (int s = 0; s < NA; ++s) {
                 r2[s] = make_float2(sr[s * 64 + lane], sr[s * 64 + 32 + lane]);
@@ -738,7 +762,7 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group 
             if (s < na) {
                 const int v = __shfl_sync(FULL, idx, s);
                 const float Lv = __ldg(g.L + size_t(v) * 2 * g.B + off);
-                const float ro = __ldcs(g.r + size_t(ab + s) * g.B + off);
+                const float ro = ((g.fresh[c] >> lane) & 1u) ? 0.0f : __ldcs(g.r + size_t(ab + s) * g.B + off);
                 x = __fsub_rn(Lv, ro);
                 chk ^= uint32_t(Lv < 0.0f);
             } else {
@@ -1070,6 +1094,241 @@ __global__ void __launch_bounds__(256) k_finalize(CodeDev cd, Group g, int nb, u
     if (fl < nb) bits_out[size_t(fl) * NW + wblk] = word;
 }
 
+// ------------------------------------------------------------------ lane refill (streaming decode, a6)
+
+// A streaming decode keeps every lane of a 64-lane group busy: a lane whose frame has
+// latched (converged, or N iterations and the final test done) is given the next frame of
+// the queue in a refill wave, while the other lanes keep iterating.  Each lane counts its
+// own iterations (lane_l); the CN kernels need no per-lane state beyond the `fresh` mask
+// (r^0 = 0 for a frame's first pass): the degree-1 decision buffers stay indexed by the
+// global pass parity, and the buffer that holds a lane's final decisions is recorded per
+// lane (lane_fbuf) when it latches.  A frame's arithmetic never depends on its lane or on
+// the other lanes, so every frame decodes bit-identically to group mode (tests).
+
+__global__ void k_stream_init(Group g) {
+    const int b = threadIdx.x;
+    if (b < g.C) {
+        g.act[b] = 0u;
+        g.unsat[b] = 0u;
+        g.invalid[b] = 0u;
+        g.fresh[b] = 0u;
+        g.newm[b] = 0u;
+        g.fin[b] = (g.B - 32 * b >= 32) ? FULL : ((1u << (g.B - 32 * b)) - 1u);   // every lane is free
+    }
+    if (b < g.B) {
+        g.lane_frame[b] = -1;
+        g.lane_l[b] = 0;
+        g.lane_fbuf[b] = 0;
+    }
+    if (b == 0) {
+        *g.iter = 1;
+        *g.done = 0;
+    }
+}
+
+// After CN pass l: per lane, latch a frame whose decisions of its iteration l_b - 1 satisfy
+// every check (ET), or whose final test (pass N + 1) is done; else count the iteration.
+// Requests a refill wave (IF node) once wave_min lanes wait or no lane iterates.
+__global__ void k_latch_stream(Group g, StreamJob* job, cudaGraphConditionalHandle if_h) {
+    __shared__ uint32_t s_act[4], s_fin[4];
+    const int b = threadIdx.x, c = b >> 5, bit = b & 31;
+    const int l = *reinterpret_cast<volatile int*>(g.iter);
+    const int N = job->N;
+    bool act = false, finished = false;
+    if (b < g.B) {
+        act = (g.act[c] >> bit) & 1u;
+        if (act) {
+            const int lb = g.lane_l[b];
+            const bool passed = !((g.unsat[c] >> bit) & 1u);
+            if (lb >= 2 && passed) {
+                g.iters[b] = lb - 1;
+                g.conv[b] = 1;
+                finished = true;
+            } else if (lb > N) {
+                g.iters[b] = N;
+                g.conv[b] = 0;
+                finished = true;
+            } else {
+                g.lane_l[b] = lb + 1;
+            }
+            if (finished) g.lane_fbuf[b] = (l - 1) & 1;   // decisions of global pass l - 1
+        }
+    }
+    const uint32_t a_bal = __ballot_sync(FULL, act && !finished), f_bal = __ballot_sync(FULL, finished);
+    if (bit == 0 && c < g.C) {
+        s_act[c] = a_bal;
+        s_fin[c] = g.fin[c] | f_bal;
+    }
+    __syncthreads();
+    if (b == 0) {
+        int nact = 0, nfin = 0;
+        for (int q = 0; q < g.C; ++q) {
+            g.act[q] = s_act[q];
+            g.fin[q] = s_fin[q];
+            g.unsat[q] = 0u;
+            g.fresh[q] = 0u;
+            nact += __popc(s_act[q]);
+            nfin += __popc(s_fin[q]);
+        }
+        cudaGraphSetConditional(if_h, (nfin > 0 && (nfin >= job->wave_min || nact == 0)) ? 1u : 0u);
+    }
+}
+
+// End of a streaming pass: advance the global pass counter; loop while any lane iterates
+// or waits for its refill wave.
+__global__ void k_stream_ctl(Group g, cudaGraphConditionalHandle while_h) {
+    *g.iter = *g.iter + 1;
+    uint32_t any = 0;
+    for (int q = 0; q < g.C; ++q) any |= g.act[q] | g.fin[q];
+    cudaGraphSetConditional(while_h, any ? 1u : 0u);
+}
+
+// Refill wave 1/4: outputs of the finished lanes (as k_finalize, per lane: frame lane_frame,
+// degree-1 decisions from buffer lane_fbuf).
+__global__ void __launch_bounds__(256) k_finalize_lanes(CodeDev cd, Group g, StreamJob* job) {
+    const int NW = (cd.n + 31) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int wblk = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int c = blockIdx.y;
+    const int b = c * 32 + lane;
+    const bool mine = (g.fin[c] >> lane) & 1u;
+    const int f = mine ? g.lane_frame[b] : -1;
+    if (f < 0) return;
+    const int it = g.iters[b];
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        job->iters[f] = it;
+        job->conv[f] = g.conv[b];
+    }
+    if (wblk >= NW) return;
+    const size_t off = size_t(c) * 32 + lane;
+    const int par = g.lane_fbuf[b];
+    uint32_t word = 0;
+    const int i0 = wblk * 32;
+    for (int ii = 0; ii < 32; ++ii) {
+        const int i = i0 + ii;
+        if (i >= cd.n) break;
+        const int v = __ldg(cd.vmap + i);
+        uint32_t bit;
+        if (v >= 0) bit = g.L[size_t(v) * 2 * g.B + off] < 0.0f;
+        else bit = (g.d1bits[(size_t(par) * cd.n_1 + ~v) * g.C + c] >> lane) & 1u;
+        word |= bit << ii;
+    }
+    if (it < 0) word = 0;
+    job->bits[size_t(f) * NW + wblk] = word;
+}
+
+// Refill wave 2/4: the finished lanes take the next frames of the queue (in lane order).
+__global__ void k_refill_assign(Group g, StreamJob* job) {
+    __shared__ int s_base;
+    __shared__ uint32_t s_new[4];
+    const int b = threadIdx.x, c = b >> 5, bit = b & 31;
+    const bool freed = b < g.B && ((g.fin[c] >> bit) & 1u);
+    uint32_t rank = 0, cnt = 0;
+    for (int q = 0; q < g.C; ++q) {
+        const uint32_t m = g.fin[q];
+        if (q < c) rank += __popc(m);
+        cnt += __popc(m);
+    }
+    if (freed) rank += __popc(g.fin[c] & ((1u << bit) - 1u));
+    if (b == 0) s_base = cnt ? atomicAdd(&job->next, int(cnt)) : 0;
+    __syncthreads();
+    const int f = s_base + int(rank);
+    const bool got = freed && f < job->nframes;
+    if (freed) {
+        g.lane_frame[b] = got ? f : -1;
+        g.lane_l[b] = got ? 1 : 0;
+    }
+    const uint32_t nb = __ballot_sync(FULL, got);
+    if (bit == 0 && c < g.C) s_new[c] = nb;
+    __syncthreads();
+    if (b < g.C) {
+        g.newm[b] = s_new[b];
+        g.fin[b] = 0u;
+        g.invalid[b] &= ~s_new[b];
+    }
+}
+
+// Refill wave 3/4: lambda of the new frames into their lanes' columns (lam_a, L = lambda,
+// accumulator 0, lam1), and their S_B bits into synd_t -- the k_scatter / k_pack_syndrome
+// transposes restricted to the new lanes.
+__global__ void __launch_bounds__(256) k_refill_scatter(CodeDev cd, Group g, StreamJob* job) {
+    __shared__ float tile[32][33];
+    const int c = blockIdx.y;
+    const uint32_t nm = g.newm[c];
+    if (!nm) return;
+    const int i0 = blockIdx.x * 32;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int rr = w; rr < 32; rr += 8) {
+        const int f = ((nm >> rr) & 1u) ? g.lane_frame[c * 32 + rr] : -1;
+        const int i = i0 + lane;
+        tile[rr][lane] = (f >= 0 && i < cd.n) ? __ldcs(job->llr + size_t(f) * cd.n + i) : 0.0f;
+    }
+    __syncthreads();
+    const size_t off = size_t(c) * 32 + lane;
+    const bool mine = (nm >> lane) & 1u;
+    for (int ii = w; ii < 32; ii += 8) {
+        const int i = i0 + ii;
+        if (i >= cd.n) break;
+        const float val = tile[lane][ii];
+        const uint32_t bad = __ballot_sync(FULL, mine && !isfinite(val));
+        if (bad && lane == 0) atomicOr(g.invalid + c, bad);
+        if (!mine) continue;
+        const int v = __ldg(cd.vmap + i);
+        if (v >= 0) {
+            g.lam_a[size_t(v) * g.B + off] = val;
+            g.L[size_t(v) * 2 * g.B + off] = val;
+            g.L[size_t(v) * 2 * g.B + g.B + off] = 0.0f;
+        } else {
+            g.lam1[size_t(~v) * g.B + off] = val;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_refill_synd(CodeDev cd, Group g, StreamJob* job) {
+    const int W = (cd.m + 31) >> 5;
+    const int lane = threadIdx.x & 31;
+    const long item = long(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (item >= long(W) * g.C) return;
+    const int wd = int(item / g.C), c = int(item % g.C);
+    const uint32_t nm = g.newm[c];
+    if (!nm) return;
+    const int f = ((nm >> lane) & 1u) ? g.lane_frame[c * 32 + lane] : -1;
+    const uint32_t word = (f >= 0) ? __ldg(job->synd + size_t(f) * W + wd) : 0u;
+    uint32_t mine = 0;
+#pragma unroll
+    for (int bb = 0; bb < 32; ++bb) {
+        const uint32_t bal = __ballot_sync(FULL, (word >> bb) & 1u);
+        if (lane == bb) mine = bal;
+    }
+    const int j = wd * 32 + lane;
+    if (j < cd.m) {
+        uint32_t* p = g.synd_t + size_t(__ldg(cd.cn_new + j)) * g.C + c;
+        *p = (*p & ~nm) | (mine & nm);
+    }
+}
+
+// Refill wave 4/4: start the new frames (fresh: r^0 = 0 in their first pass); a frame with a
+// non-finite LLR is not decoded (iterations = -1, R24) and waits for the next wave's outputs.
+__global__ void k_refill_activate(Group g) {
+    const int b = threadIdx.x, c = b >> 5, bit = b & 31;
+    if (b >= g.B) return;
+    const uint32_t nm = g.newm[c];
+    if (!((nm >> bit) & 1u)) return;
+    const bool bad = (g.invalid[c] >> bit) & 1u;
+    if (bad) {
+        g.iters[b] = -1;
+        g.conv[b] = 0;
+        g.lane_fbuf[b] = 0;
+        atomicOr(g.fin + c, 1u << bit);
+    } else {
+        g.iters[b] = 0;
+        g.conv[b] = 0;
+        atomicOr(g.act + c, 1u << bit);
+        atomicOr(g.fresh + c, 1u << bit);
+    }
+    atomicAnd(g.newm + c, ~(1u << bit));
+}
+
 // ------------------------------------------------------------------ LLR from MD output (a1, R13)
 
 __global__ void __launch_bounds__(256) k_md_llr(int64_t total, int n, int d, float c, const float* __restrict__ v,
@@ -1309,6 +1568,25 @@ void launch_pack_syndrome(const CodeDev& cd, const Group& g, const uint32_t* syn
 void launch_init_ctl(const Group& g, int nb, int N, cudaStream_t s) { k_init_ctl<<<1, 128, 0, s>>>(g, nb, N); }
 
 void launch_latch_dev(const Group& g, bool et, cudaStream_t s) { k_latch_dev<<<1, 32, 0, s>>>(g, et ? 1 : 0); }
+
+void launch_stream_init(const Group& g, cudaStream_t s) { k_stream_init<<<1, 128, 0, s>>>(g); }
+
+void launch_latch_stream(const Group& g, StreamJob* job, unsigned long long if_handle, cudaStream_t s) {
+    k_latch_stream<<<1, 128, 0, s>>>(g, job, cudaGraphConditionalHandle(if_handle));
+}
+
+void launch_stream_ctl(const Group& g, unsigned long long while_handle, cudaStream_t s) {
+    k_stream_ctl<<<1, 1, 0, s>>>(g, cudaGraphConditionalHandle(while_handle));
+}
+
+void launch_refill_wave(const CodeDev& cd, const Group& g, StreamJob* job, cudaStream_t s) {
+    const int NW = (cd.n + 31) / 32, W = (cd.m + 31) / 32;
+    k_finalize_lanes<<<dim3((NW + 7) / 8, g.C), 256, 0, s>>>(cd, g, job);
+    k_refill_assign<<<1, 128, 0, s>>>(g, job);
+    k_refill_scatter<<<dim3((cd.n + 31) / 32, g.C), 256, 0, s>>>(cd, g, job);
+    k_refill_synd<<<unsigned((long(W) * g.C + 7) / 8), 256, 0, s>>>(cd, g, job);
+    k_refill_activate<<<1, 128, 0, s>>>(g);
+}
 
 void launch_loop_ctl(const Group& g, unsigned long long cond_handle, cudaStream_t s) {
     k_loop_ctl<<<1, 1, 0, s>>>(g, cudaGraphConditionalHandle(cond_handle));

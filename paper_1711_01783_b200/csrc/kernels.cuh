@@ -28,6 +28,27 @@ struct Group {
     int32_t* done;     // [1]  all lanes latched
     int32_t* iter;     // [1]  current iteration l (graph-driven loop; 1-based)
     int32_t* maxit;    // [1]  N of the running decode
+    // lane refill (streaming decode; all zero / unused in group mode)
+    uint32_t* fresh;   // [C]  lanes whose frame starts in this pass: r^0 = 0 (Step 2)
+    uint32_t* fin;     // [C]  lanes whose frame finished and awaits the refill wave
+    uint32_t* newm;    // [C]  lanes given a new frame by the running refill wave
+    int32_t* lane_l;   // [B]  pass number of the lane's current frame (its iteration l)
+    int32_t* lane_frame;  // [B] frame index of the lane in the batch (-1: none)
+    int32_t* lane_fbuf;   // [B] d1bits buffer holding the lane's final degree-1 decisions
+};
+
+// Frame queue of a streaming decode (device memory, shared by the K workspaces): the
+// batch's buffers, the next unassigned frame and the refill threshold.
+struct StreamJob {
+    const float* llr;      // [nframes][n]
+    const uint32_t* synd;  // [nframes][W]
+    uint32_t* bits;        // [nframes][NW]
+    int32_t* iters;        // [nframes]
+    uint8_t* conv;         // [nframes]
+    int32_t nframes;
+    int32_t next;          // atomically advanced by the refill waves
+    int32_t N;             // max_iter
+    int32_t wave_min;      // refill once this many lanes have finished (or none iterates)
 };
 
 struct CodeDev {
@@ -66,6 +87,11 @@ void launch_init_ctl(const Group& g, int nb, int N, cudaStream_t s);
 // Device-driven iteration control for the CUDA-graph loop (l read from Group::iter).
 void launch_latch_dev(const Group& g, bool et, cudaStream_t s);
 void launch_loop_ctl(const Group& g, unsigned long long cond_handle, cudaStream_t s);
+// lane refill (streaming decode)
+void launch_stream_init(const Group& g, cudaStream_t s);
+void launch_latch_stream(const Group& g, StreamJob* job, unsigned long long if_handle, cudaStream_t s);
+void launch_stream_ctl(const Group& g, unsigned long long while_handle, cudaStream_t s);
+void launch_refill_wave(const CodeDev& cd, const Group& g, StreamJob* job, cudaStream_t s);
 // l >= 1: iteration given by the host; l == 0: read from Group::iter (graph body), with
 // et telling whether iterations >= 2 test the syndrome.
 void launch_cn(const CodeDev& cd, const Group& g, int rule, int D, int nd, int begin, int count, int ts, int grid,

@@ -184,6 +184,36 @@ def test_ragged_batch_max_batch_and_host_path(c1):
         _assert_frame_equal(code, o, bits[i], iters[i], conv[i])
 
 
+@pytest.mark.parametrize("rule,groups,wave", [(B.RULE_EXACT, 2, "16"), (B.RULE_PHI_LUT, 1, "1"), (B.RULE_EXACT, 3, "40")])
+def test_lane_refill_streaming_bit_exact(c1, rule, groups, wave, monkeypatch):
+    """Lane refill (metldpc_config_t.lane_refill, streaming decode): 301 frames (a ragged
+    batch: 4 x 64 + 45) at SNRs from 0.16 to 0.6, so lanes latch at very different
+    iterations and are refilled from the queue while others iterate; one frame has a
+    non-finite LLR and one is noiseless.  Every frame's bits, iteration count and flag equal
+    the oracle's and the group-mode decode's, for several refill thresholds."""
+    monkeypatch.setenv("METLDPC_REFILL_MIN", wave)
+    code, h = c1
+    fr = _frames(code, [(0.16, 60), (0.2, 80), (0.3, 80), (0.6, 81)], key=11)
+    llr = _llr_oracle(fr)
+    llr[5, 100] = np.nan
+    llr[7] = ((1.0 - 2.0 * fr["u"][7]) * 8.0).astype(np.float32)
+    nb = llr.shape[0]
+    dec = B.Decoder(h, nb, rule=rule, max_iter=60, groups_in_flight=groups, lane_refill=True)
+    bits, iters, conv = dec.decode(torch.from_numpy(llr).cuda(), torch.from_numpy(fr["synd"].view(np.int32)).cuda())
+    torch.cuda.synchronize()
+    bits, iters, conv = bits.cpu().numpy().view(np.uint32), iters.cpu().numpy(), conv.cpu().numpy()
+    _, gb, gi, gc = _gpu_decode(h, llr, fr["synd"], rule, 60, groups=groups)
+    assert np.array_equal(bits, gb) and np.array_equal(iters, gi) and np.array_equal(conv, gc)
+    assert iters[5] == -1 and conv[5] == 0 and not bits[5].any()
+    assert iters[7] == 1 and conv[7] == 1
+    assert len(set(iters.tolist())) > 10          # lanes really latch at many different iterations
+    for i in list(range(0, nb, 7)) + [nb - 1]:
+        if i == 5:
+            continue
+        o = bp.decode(code, llr[i], fr["synd"][i], 60, early_term=True, rule=rule, prec=32)
+        _assert_frame_equal(code, o, bits[i], iters[i], conv[i], f"frame {i}")
+
+
 def test_edge_cases(c1):
     """Zero noise -> l = 1, c = u; non-finite LLR -> iterations -1 (R24) without
     disturbing neighbours; max_iter = 1; empty batch."""
