@@ -65,7 +65,8 @@ def parse():
     ap.add_argument("--distinct", type=int, default=64, help="distinct frames generated per rank (tiled)")
     ap.add_argument("--rule", choices=["exact", "lut"], default="exact")
     ap.add_argument("--no-et", action="store_true")
-    ap.add_argument("--refill", action="store_true", help="lane refill (streaming decode, metldpc_config_t.lane_refill)")
+    ap.add_argument("--no-refill", action="store_true",
+                    help="group mode instead of lane refill (metldpc_config_t.lane_refill = 0)")
     ap.add_argument("--no-skip", action="store_true",
                     help="iterate degree-1 VNs too (Table 1 'without skipping', METLDPC_CODE_NO_SKIP)")
     ap.add_argument("--lanes", type=int, default=64)
@@ -259,7 +260,7 @@ def main():
     hc = B.Code(code, device=local, no_skip=a.no_skip)
     st = dict(st, iter_edges=hc.info.iter_edges, n_deg1=hc.info.n_deg1, n_active=hc.info.n_active)
     dec = B.Decoder(hc, F, rule=_rule(a), max_iter=a.iters, early_term=not a.no_et, lanes_per_group=a.lanes,
-                    groups_in_flight=a.groups, lane_refill=a.refill)
+                    groups_in_flight=a.groups, lane_refill=not a.no_refill)
     llr = torch.empty_like(v)
     nw = (a.n + 31) // 32
     bits = torch.empty((F, nw), dtype=torch.int32, device=dev)
@@ -388,6 +389,7 @@ def main():
                        "beta": metrics.beta(R, a.snr), "max_iter": a.iters, "early_term": not a.no_et,
                        "rule": a.rule.upper(), "frames_per_gpu": F, "distinct_frames_per_gpu": ND,
                        "lanes_per_group": a.lanes, "groups_in_flight": a.groups, "global_batch": F * world,
+                       "lane_refill": not a.no_refill,
                        "l2": "inputs larger than L2 (v 1 GB, edge messages 740 MB per 64-lane group)",
                        "parallelism": f"dp{world} (frames sharded f mod G; NCCL all-reduce of FER counters)"},
             "baseline_context": (f"vs_baseline = value / {paper_mbps(a)} Mb/s: paper Table 1 rate "

@@ -67,7 +67,9 @@ typedef struct {
                                   whose frame has latched takes the next frame of the batch in
                                   a refill wave while the other lanes keep iterating, so a
                                   group no longer waits for its slowest frame; per-frame
-                                  results are identical to group mode.  Default 0.           */
+                                  results are identical to group mode.  Default 1 (used by
+                                  metldpc_decode when early_term and lanes_per_group = 64;
+                                  the host-buffer calls and profiling use group mode).     */
 } metldpc_config_t;
 
 typedef struct {
@@ -196,7 +198,9 @@ metldpc_status metldpc_syndrome(metldpc_decoder dec, int32_t batch, const uint32
  *                                value (R24; bits are then 0)
  *   converged_out dev u8 [batch] 1 iff H c = S_B for the returned c
  * Results are latched per frame at the first syndrome match (R12), so they do not
- * depend on batch composition, lane, group size or device. 0 <= batch <= max_batch. */
+ * depend on batch composition, lane, group size, device or lane refill (cfg.lane_refill:
+ * frames stream through the lanes, each freed lane taking the next frame of the batch).
+ * 0 <= batch <= max_batch. */
 metldpc_status metldpc_decode(metldpc_decoder dec, int32_t batch,
                               const float* llr, const uint32_t* syndrome, int32_t max_iter,
                               uint32_t* bits_out, int32_t* iters_out, uint8_t* converged_out,

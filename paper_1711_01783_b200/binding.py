@@ -282,12 +282,13 @@ class Decoder:
 
     def __init__(self, code: Code, max_batch: int, rule: int = RULE_EXACT, max_iter: int = 100,
                  early_term: bool = True, lanes_per_group: int = 64, groups_in_flight: int | None = None,
-                 lane_refill: bool = False):
+                 lane_refill: bool | None = None):
         cfg = metldpc_config_default()
         cfg.rule, cfg.max_iter, cfg.early_term, cfg.lanes_per_group = rule, max_iter, int(early_term), lanes_per_group
         if groups_in_flight is not None:
             cfg.groups_in_flight = groups_in_flight
-        cfg.lane_refill = int(lane_refill)
+        if lane_refill is not None:
+            cfg.lane_refill = int(lane_refill)
         self.cfg = cfg
         self.code = code
         self.max_batch = max_batch

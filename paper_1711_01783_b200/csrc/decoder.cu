@@ -62,6 +62,7 @@ struct metldpc_decoder_s {
     std::vector<cudaGraphExec_t> loop_exec;
     std::vector<cudaGraphExec_t> stream_exec;       // lane-refill graph per workspace
     StreamJob* job = nullptr;                       // frame queue of a streaming decode (device)
+    bool stream_used = false;                       // a streaming decode ran (device-side counters)
     int use_graph = 1;
     std::vector<cudaStream_t> gs;                   // one stream per workspace (K > 1)
     std::vector<cudaEvent_t> fork_ev, join_ev;
@@ -150,6 +151,7 @@ Group group_of(metldpc_decoder d, int k) {
     g.lane_l = w.lane_l;
     g.lane_frame = w.lane_frame;
     g.lane_fbuf = w.lane_fbuf;
+    g.stat = w.ctl + 14;
     return g;
 }
 
@@ -467,7 +469,8 @@ metldpc_status stream_decode(metldpc_decoder d, int32_t batch, const float* llr,
         launch_stream_init(g, ks);
         launch_refill_wave(cd, g, d->job, ks);   // first fill
         CUDA_TRY(cudaGraphLaunch(exec, ks));
-        d->prof.launches += 6;
+        d->prof.launches += 1;                   // + passes and waves, counted on the device
+        d->stream_used = true;
         d->last_ws = k;
     }
     if (K > 1)
@@ -601,6 +604,7 @@ void metldpc_config_default(metldpc_config_t* cfg) {
     cfg->early_term = 1;
     cfg->lanes_per_group = 64;
     cfg->groups_in_flight = 4;
+    cfg->lane_refill = 1;
 }
 
 metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, const metldpc_config_t* cfg_in,
@@ -1073,6 +1077,19 @@ metldpc_status metldpc_get_profile(metldpc_decoder d, metldpc_profile_t* out) {
     if (!d || !out) return fail(METLDPC_EINVAL, "NULL argument");
     ev_collect(d);
     *out = d->prof;
+    if (d->stream_used) {   // streaming passes / waves are counted on the device
+        CUDA_TRY(cudaDeviceSynchronize());
+        size_t per_pass = 3;   // latch, finish, loop control
+        for (const auto& c : d->cn_classes) per_pass += 1;
+        for (const auto& w : d->ws) {
+            uint32_t st[2] = {0, 0};
+            CUDA_TRY(cudaMemcpy(st, w.ctl + 14, sizeof(st), cudaMemcpyDeviceToHost));
+            out->launches += int64_t(st[0]) * int64_t(per_pass) + int64_t(st[1]) * 5;
+            out->cn_launches += st[0];
+            out->vn_launches += st[0];
+            out->cn_lane_iters += int64_t(st[0]) * d->B;
+        }
+    }
     return METLDPC_OK;
 }
 
@@ -1080,6 +1097,10 @@ metldpc_status metldpc_reset_profile(metldpc_decoder d) {
     if (!d) return fail(METLDPC_EINVAL, "NULL decoder");
     ev_collect(d);
     d->prof = metldpc_profile_t{};
+    if (d->stream_used) {
+        CUDA_TRY(cudaDeviceSynchronize());
+        for (const auto& w : d->ws) CUDA_TRY(cudaMemset(w.ctl + 14, 0, 2 * sizeof(uint32_t)));
+    }
     return METLDPC_OK;
 }
 

@@ -1178,6 +1178,7 @@ __global__ void k_latch_stream(Group g, StreamJob* job, cudaGraphConditionalHand
 // or waits for its refill wave.
 __global__ void k_stream_ctl(Group g, cudaGraphConditionalHandle while_h) {
     *g.iter = *g.iter + 1;
+    g.stat[0] += 1u;
     uint32_t any = 0;
     for (int q = 0; q < g.C; ++q) any |= g.act[q] | g.fin[q];
     cudaGraphSetConditional(while_h, any ? 1u : 0u);
@@ -1311,6 +1312,7 @@ __global__ void __launch_bounds__(256) k_refill_synd(CodeDev cd, Group g, Stream
 // non-finite LLR is not decoded (iterations = -1, R24) and waits for the next wave's outputs.
 __global__ void k_refill_activate(Group g) {
     const int b = threadIdx.x, c = b >> 5, bit = b & 31;
+    if (b == 0) g.stat[1] += 1u;
     if (b >= g.B) return;
     const uint32_t nm = g.newm[c];
     if (!((nm >> bit) & 1u)) return;

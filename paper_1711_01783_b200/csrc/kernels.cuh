@@ -35,6 +35,7 @@ struct Group {
     int32_t* lane_l;   // [B]  pass number of the lane's current frame (its iteration l)
     int32_t* lane_frame;  // [B] frame index of the lane in the batch (-1: none)
     int32_t* lane_fbuf;   // [B] d1bits buffer holding the lane's final degree-1 decisions
+    uint32_t* stat;    // [2]  streaming passes and refill waves run (kernel-launch accounting)
 };
 
 // Frame queue of a streaming decode (device memory, shared by the K workspaces): the

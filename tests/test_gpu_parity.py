@@ -40,9 +40,9 @@ def _llr_oracle(fr):
     return np.stack([bp.llr_from_md_f32(fr["v"][i], fr["xnorm"][i], fr["snr"][i]) for i in range(len(fr["v"]))])
 
 
-def _gpu_decode(code_h, llr, synd, rule, max_iter, et=True, lanes=64, max_batch=None, groups=None):
+def _gpu_decode(code_h, llr, synd, rule, max_iter, et=True, lanes=64, max_batch=None, groups=None, refill=None):
     dec = B.Decoder(code_h, max_batch or llr.shape[0], rule=rule, max_iter=max_iter, early_term=et,
-                    lanes_per_group=lanes, groups_in_flight=groups)
+                    lanes_per_group=lanes, groups_in_flight=groups, lane_refill=refill)
     bits, iters, conv = dec.decode(torch.from_numpy(llr).cuda(), torch.from_numpy(synd.view(np.int32)).cuda())
     torch.cuda.synchronize()
     return dec, bits.cpu().numpy().view(np.uint32), iters.cpu().numpy(), conv.cpu().numpy()
@@ -146,23 +146,25 @@ def test_no_skip_variant_bit_exact(c1, rule):
 
 @pytest.mark.parametrize("et", [True, False])
 def test_batch_lane_and_group_invariance(c1, et):
-    """S:220 / R12: a frame's result does not depend on batch size, lane or group size."""
+    """S:220 / R12: a frame's result does not depend on batch size, lane, group size or
+    lane refill (streaming decode vs group mode)."""
     code, h = c1
     fr = _frames(code, [(0.161, 30), (0.3, 40), (0.6, 30)])
     llr = _llr_oracle(fr)
     ref = None
-    for lanes, groups in ((32, 1), (64, 1), (64, 2), (64, 3), (128, 2)):
+    for lanes, groups, refill in ((32, 1, None), (64, 1, False), (64, 1, True), (64, 2, True), (64, 3, False),
+                                  (128, 2, None)):
         for order in ("fwd", "rev"):
             idx = np.arange(len(llr)) if order == "fwd" else np.arange(len(llr))[::-1].copy()
             _, bits, iters, conv = _gpu_decode(h, llr[idx], fr["synd"][idx], B.RULE_EXACT, 60, et=et, lanes=lanes,
-                                               groups=groups)
+                                               groups=groups, refill=refill)
             inv = np.argsort(idx)
             res = (bits[inv], iters[inv], conv[inv])
             if ref is None:
                 ref = res
             else:
                 for a, b in zip(ref, res):
-                    assert np.array_equal(a, b), (lanes, groups, order)
+                    assert np.array_equal(a, b), (lanes, groups, refill, order)
     # single-frame batches agree too
     for i in (0, 45, 99):
         _, bits, iters, conv = _gpu_decode(h, llr[i:i + 1], fr["synd"][i:i + 1], B.RULE_EXACT, 60, et=et)
@@ -202,7 +204,7 @@ def test_lane_refill_streaming_bit_exact(c1, rule, groups, wave, monkeypatch):
     bits, iters, conv = dec.decode(torch.from_numpy(llr).cuda(), torch.from_numpy(fr["synd"].view(np.int32)).cuda())
     torch.cuda.synchronize()
     bits, iters, conv = bits.cpu().numpy().view(np.uint32), iters.cpu().numpy(), conv.cpu().numpy()
-    _, gb, gi, gc = _gpu_decode(h, llr, fr["synd"], rule, 60, groups=groups)
+    _, gb, gi, gc = _gpu_decode(h, llr, fr["synd"], rule, 60, groups=groups, refill=False)
     assert np.array_equal(bits, gb) and np.array_equal(iters, gi) and np.array_equal(conv, gc)
     assert iters[5] == -1 and conv[5] == 0 and not bits[5].any()
     assert iters[7] == 1 and conv[7] == 1

@@ -32,7 +32,7 @@ def main():
     ap.add_argument("--key", type=int, default=5)
     ap.add_argument("--out", default=None)
     ap.add_argument("--groups", type=int, default=4, help="lane groups in flight")
-    ap.add_argument("--refill", action="store_true", help="lane refill (streaming decode)")
+    ap.add_argument("--no-refill", action="store_true", help="group mode instead of lane refill")
     a = ap.parse_args()
 
     import torch
@@ -48,7 +48,7 @@ def main():
     R = (st["n"] - st["m"]) / st["n"]
     h = B.Code(code)
     dec = B.Decoder(h, a.batch, rule=0 if a.rule == "exact" else 1, max_iter=a.iters, groups_in_flight=a.groups,
-                    lane_refill=a.refill)
+                    lane_refill=not a.no_refill)
     out = open(a.out, "w") if a.out else None
     for snr in [float(s) for s in a.snrs.split(",")]:
         frames = conv = undet = iters_sum = 0
@@ -80,7 +80,7 @@ def main():
                 hist[min(max(v, 0), a.iters)] += 1
         rec = {"config": "C5", "family": a.family, "n": a.n, "snr": snr, "beta": metrics.beta(R, snr),
                "max_iter": a.iters, "rule": a.rule.upper(), "batch": a.batch, "groups": a.groups,
-               "lane_refill": a.refill, "frames": frames, "fer": 1.0 - conv / frames,
+               "lane_refill": not a.no_refill, "frames": frames, "fer": 1.0 - conv / frames,
                "undetected_rate": undet / frames, "mean_iters": iters_sum / frames,
                "decode_mbps": frames * a.n / (dev_ms / 1e3) / 1e6,
                "iter_hist": {str(k): v for k, v in enumerate(hist) if v}}
