@@ -332,6 +332,9 @@ __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 
 // two independent dependency chains), for larger NA one chunk per unit (register budget).
 // The tile's metadata is one coalesced load per array and its active-edge VN indices
 // (pre-scaled to row offsets) are staged in shared memory.
+#ifndef METLDPC_PAIR_MAX_NA
+#define METLDPC_PAIR_MAX_NA 4   // largest active count run two lanes per thread in k_cn_tile
+#endif
 template <int NA>
 __host__ __device__ constexpr int cn_tile_min_blocks() { return NA <= 4 ? 2 : 1; }   // NA > 4: 128 registers
 
@@ -339,7 +342,7 @@ template <int RULE, int NA, int ND>
 __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_tile(CodeDev cd, Group g, CnCtl karg,
                                                                                   int begin, int count, int ts) {
     using PT = PhiT<RULE>;
-    constexpr int LPT = (NA <= 4) ? 2 : 1;     // lanes per thread
+    constexpr int LPT = (NA <= METLDPC_PAIR_MAX_NA) ? 2 : 1;     // lanes per thread
     constexpr int UPT = 2 / LPT;               // units per tile
     constexpr int NAS = NA > 0 ? NA : 1;
     constexpr int STAGE = (NA <= 4 ? 32 : 8) * NAS;
@@ -399,7 +402,7 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
 #pragma unroll
                 for (int s = 0; s < NA; ++s) {
                     const int o = idx[s];
-                    if constexpr (NA <= 4) offs[s] = uint32_t(o) + lo;
+                    if constexpr (NA <= 4 || LPT == 2) offs[s] = uint32_t(o) + lo;
 #pragma unroll
                     for (int h = 0; h < LPT; ++h) {
                         Lv[h][s] = (NA <= 4) ? __ldg(g.L + offs[s] + h * 32) : __ldg(pL + o + h * 32);
@@ -1524,7 +1527,7 @@ static void cn_pipe_geom(int rule, int D, int nd, int* threads, size_t* smem) {
 }
 
 int cn_tile_max(int D, int nd) { return (D - nd) <= 4 ? 32 : 8; }
-int cn_units_per_tile(int D, int nd) { return (D - nd) <= 4 ? 1 : 2; }
+int cn_units_per_tile(int D, int nd) { return (D - nd) <= METLDPC_PAIR_MAX_NA ? 1 : 2; }
 
 size_t cn_smem(int rule, int D, int nd) {
     const size_t tab = size_t(rule == METLDPC_RULE_EXACT ? PhiT<METLDPC_RULE_EXACT>::TAB_BYTES
