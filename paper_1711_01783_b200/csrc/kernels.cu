@@ -327,13 +327,15 @@ __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 
 #endif
 
 // One degree class (CN labels [begin, begin + count), NA active + ND <= 1 degree-1 slots)
-// for 64-lane groups.  Work unit = a tile of ts consecutive CNs owned by one warp; for
-// NA <= 4 the warp covers both 32-lane chunks (each thread: lanes `lane` and `lane + 32`,
-// two independent dependency chains), for larger NA one chunk per unit (register budget).
+// for 64-lane groups.  Work unit = a tile of ts consecutive CNs owned by one warp that
+// covers both 32-lane chunks (each thread: lanes `lane` and `lane + 32`, two independent
+// dependency chains; NA > 4 runs 1 CTA per SM with up to 128 registers).  With
+// METLDPC_PAIR_MAX_NA < NA a unit is one chunk instead (the latency-bound core classes
+// measured ~2 % faster with two lanes per thread).
 // The tile's metadata is one coalesced load per array and its active-edge VN indices
 // (pre-scaled to row offsets) are staged in shared memory.
 #ifndef METLDPC_PAIR_MAX_NA
-#define METLDPC_PAIR_MAX_NA 4   // largest active count run two lanes per thread in k_cn_tile
+#define METLDPC_PAIR_MAX_NA 16  // largest active count run two lanes per thread in k_cn_tile
 #endif
 template <int NA>
 __host__ __device__ constexpr int cn_tile_min_blocks() { return NA <= 4 ? 2 : 1; }   // NA > 4: 128 registers
@@ -519,7 +521,11 @@ struct PipeCfg {
                                    ? PhiT<METLDPC_RULE_EXACT>::TAB_BYTES
                                    : PhiT<METLDPC_RULE_PHI_LUT>::TAB_BYTES;
     static constexpr int W0 = (kSmemPerSm - TAB - 64) / WARP_BYTES;
+#ifdef METLDPC_PIPE_WMAX
+    static constexpr int WMAX = METLDPC_PIPE_WMAX;
+#else
     static constexpr int WMAX = METLDPC_PIPE_LREG ? 24 : 32;          // L prefetch in registers: 80 regs
+#endif
     static constexpr int WARPS = W0 > WMAX ? WMAX : W0;
     static constexpr int THREADS = WARPS * 32;
 };
