@@ -342,7 +342,7 @@ def main():
     it_bytes = F * world * a.steps * a.iters
     roofline = {"bound": "hbm", "achieved": cn_gbs, "peak": peak, "unit": "GB/s",
                 "frac": (cn_gbs / peak) if cn_gbs else None, "traffic": traffic,
-                "kernel": "k_cn_update (all CN degree classes of one iteration)",
+                "kernel": "CN phase: k_cn_pipe + k_cn_tile launches of one iteration (all degree classes, VN sums fused)",
                 "bytes_per_launch": bm["cn"] * min(F, a.lanes), "peak_source": peak_src,
                 "avg_launch_ms": prof_k["cn_ms"] / max(1, prof_k["cn_launches"]), "kernel_timing": kernel_timing,
                 "vn_update": {"achieved": vn_gbs, "frac": (vn_gbs / peak) if vn_gbs else None,

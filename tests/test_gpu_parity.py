@@ -216,6 +216,25 @@ def test_lane_refill_streaming_bit_exact(c1, rule, groups, wave, monkeypatch):
         _assert_frame_equal(code, o, bits[i], iters[i], conv[i], f"frame {i}")
 
 
+def test_lane_refill_edge_cases(c1):
+    """Streaming decode corner cases: fewer frames than lanes, max_iter = 1 (every frame's
+    final test is its second pass), and a queue of noiseless frames that all latch at l = 1
+    so every lane is refilled every other pass; each against group mode."""
+    code, h = c1
+    fr = _frames(code, [(0.25, 140)], key=23)
+    llr = _llr_oracle(fr)
+    clean = ((1.0 - 2.0 * fr["u"]) * 8.0).astype(np.float32)
+    for x, nf, N in ((llr, 5, 40), (llr, 140, 1), (clean, 140, 30)):
+        a = _gpu_decode(h, x[:nf], fr["synd"][:nf], B.RULE_EXACT, N, refill=True, groups=2)[1:]
+        b = _gpu_decode(h, x[:nf], fr["synd"][:nf], B.RULE_EXACT, N, refill=False, groups=2)[1:]
+        for u, v in zip(a, b):
+            assert np.array_equal(u, v), (nf, N)
+    _, bits, iters, conv = _gpu_decode(h, clean, fr["synd"], B.RULE_EXACT, 30, refill=True)
+    assert (iters == 1).all() and conv.all()
+    for i in range(0, 140, 13):
+        assert np.array_equal(unpack_bits(bits[i], code.n), fr["u"][i])
+
+
 def test_edge_cases(c1):
     """Zero noise -> l = 1, c = u; non-finite LLR -> iterations -1 (R24) without
     disturbing neighbours; max_iter = 1; empty batch."""
