@@ -70,7 +70,7 @@ def parse():
     ap.add_argument("--no-skip", action="store_true",
                     help="iterate degree-1 VNs too (Table 1 'without skipping', METLDPC_CODE_NO_SKIP)")
     ap.add_argument("--lanes", type=int, default=64)
-    ap.add_argument("--groups", type=int, default=4, help="lane groups decoded concurrently per GPU")
+    ap.add_argument("--groups", type=int, default=2, help="lane groups decoded concurrently per GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle work for cpu_baseline")

@@ -603,7 +603,7 @@ void metldpc_config_default(metldpc_config_t* cfg) {
     cfg->max_iter = 100;
     cfg->early_term = 1;
     cfg->lanes_per_group = 64;
-    cfg->groups_in_flight = 4;
+    cfg->groups_in_flight = 2;
     cfg->lane_refill = 1;
 }
 
