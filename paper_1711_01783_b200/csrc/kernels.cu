@@ -490,43 +490,28 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
 
 // Exact-degree classes with 1..4 active slots and <= 1 degree-1 slot (at C3: 97 % of the
 // CNs, all of the inner checks) for 64-lane groups.  Same arithmetic as k_cn_tile (cn_pair),
-// different data movement: every input of a CN arrives in shared memory by TMA while the
-// warp computes the previous CN.  In an exact-degree class CN j owns r rows abase +
-// (j - begin) NA .. + NA and lambda row dbase + (j - begin), and its active VNs' posterior
-// rows are L + a_vn * 128 (256 bytes each); one lane per warp issues 1D bulk copies
-// (cp.async.bulk, no registers held) of those 2 NA + ND rows into a 2-stage ring completing
-// on an mbarrier, so a warp always has the next CN's DRAM and L2 traffic in flight.  The
-// tile's VN row offsets are staged one tile ahead (double buffer) so the producer can run
-// into the next tile.  One CTA per SM shares a single phi table; its warp count is what
-// the rings leave room for.
+// different data movement.  In an exact-degree class CN j owns r rows abase + (j - begin) NA
+// .. + NA and lambda row dbase + (j - begin), so a warp's DRAM stream is known in advance:
+// one lane per warp issues 1D bulk copies (cp.async.bulk on the TMA unit, no registers held,
+// evict-first L2 policy) of the next CN's NA + ND rows into a 2-stage shared-memory ring that
+// completes on an mbarrier, while the warp computes the current CN from the previous stage.
+// The L gathers stay direct loads (L2 hits; staging them by TMA as well, prefetching them
+// into registers or L1 all measured slower -- DESIGN.md section 7).  The tile's VN row offsets
+// are staged one tile ahead (double buffer).  One CTA per SM shares a single phi table; its
+// warp count is what the rings leave room for.
 constexpr int kPipeStages = 2;
 constexpr int kSmemPerSm = 232448;     // opt-in dynamic shared memory per block (227 KB)
-#ifndef METLDPC_PIPE_L
-#define METLDPC_PIPE_L 0   // 1: the L rows also come by TMA (measured slower: 0.59 vs 0.54 ms at C3)
-#endif
-#ifndef METLDPC_PIPE_LPF
-#define METLDPC_PIPE_LPF 0    // CNs of look-ahead for an L1 prefetch of the L lines (0: off)
-#endif
-#ifndef METLDPC_PIPE_LREG
-#define METLDPC_PIPE_LREG 0   // 1: the next CN's L gathers are issued into registers one CN ahead
-#endif
 
 template <int NA, int ND>
 struct PipeCfg {
-    static constexpr int NL = METLDPC_PIPE_L ? NA : 0;                // staged posterior rows
-    static constexpr int STG = (NA + ND + NL) * 256;                  // bytes per stage: r, lambda[, L]
+    static constexpr int STG = (NA + ND) * 256;                       // bytes per stage: r, lambda
     static constexpr int IDX = 32 * NA;                               // ints per staged tile
     static constexpr int WARP_BYTES = 2 * IDX * 4 + kPipeStages * STG + kPipeStages * 8;
     static constexpr int TAB = (PhiT<METLDPC_RULE_EXACT>::TAB_BYTES > PhiT<METLDPC_RULE_PHI_LUT>::TAB_BYTES)
                                    ? PhiT<METLDPC_RULE_EXACT>::TAB_BYTES
                                    : PhiT<METLDPC_RULE_PHI_LUT>::TAB_BYTES;
     static constexpr int W0 = (kSmemPerSm - TAB - 64) / WARP_BYTES;
-#ifdef METLDPC_PIPE_WMAX
-    static constexpr int WMAX = METLDPC_PIPE_WMAX;
-#else
-    static constexpr int WMAX = METLDPC_PIPE_LREG ? 24 : 32;          // L prefetch in registers: 80 regs
-#endif
-    static constexpr int WARPS = W0 > WMAX ? WMAX : W0;
+    static constexpr int WARPS = W0 > 32 ? 32 : W0;
     static constexpr int THREADS = WARPS * 32;
 };
 
@@ -557,11 +542,6 @@ __device__ __forceinline__ void tma_load_1d_ef(uint32_t dst, const void* src, ui
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
         "l"(src), "r"(bytes), "r"(bar), "l"(pol)
         : "memory");
-}
-__device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                 "l"(src), "r"(bytes), "r"(bar)
-                 : "memory");
 }
 
 template <int RULE, int NA, int ND>
@@ -604,8 +584,8 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND>::THREADS, 1)
         const int jt = tile * TS, nt = min(TS, count - jt);
         for (int e = lane; e < nt * NA; e += 32) s_idx[b * PC::IDX + e] = __ldg(cd.a_vn + abase + jt * NA + e) * 128;
     };
-    // producer cursor (tile, index, idx buffer) runs kPipeStages - 1 CNs ahead of the consumer
-    int pt = gw, pi = 0, pb = 0;
+    // producer cursor (tile, index) runs kPipeStages - 1 CNs ahead of the consumer
+    int pt = gw, pi = 0;
     uint32_t np = 0, nc = 0;
     auto produce = [&]() {
         if (pt >= ntiles) return;
@@ -616,14 +596,9 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND>::THREADS, 1)
             mbar_expect_tx(bar, PC::STG);
             tma_load_1d_ef(dst, g.r + size_t(abase + jl * NA) * 64, NA * 256, bar, pol);
             if constexpr (ND > 0) tma_load_1d_ef(dst + NA * 256, g.lam1 + size_t(dbase + jl) * 64, 256, bar, pol);
-            if constexpr (PC::NL > 0) {
-                const int* ix = s_idx + pb * PC::IDX + pi * NA;
-#pragma unroll
-                for (int s = 0; s < NA; ++s) tma_load_1d(dst + (NA + ND + s) * 256, g.L + ix[s], 256, bar);
-            }
         }
         ++np;
-        if (++pi == min(TS, count - pt * TS)) { pi = 0; pt += GW; pb ^= 1; }
+        if (++pi == min(TS, count - pt * TS)) { pi = 0; pt += GW; }
     };
     if (gw < ntiles) stage_idx(gw, 0);
     __syncwarp();
@@ -642,26 +617,8 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND>::THREADS, 1)
             if (k.check && on)
                 wv_l = __ldg(reinterpret_cast<const uint2*>(g.d1bits) + (size_t(k.rpar) * cd.n_1 + dbase + jt + lane));
         __syncwarp();
-        float2 Lnx[NA];   // METLDPC_PIPE_LREG: L of CN i, gathered during CN i - 1
-        if constexpr (METLDPC_PIPE_LREG && PC::NL == 0) {
-            const int* ix = s_idx + cb * PC::IDX;
-#pragma unroll
-            for (int s = 0; s < NA; ++s) {
-                const uint32_t o = uint32_t(ix[s]) + uint32_t(lane);
-                Lnx[s] = make_float2(__ldg(g.L + o), __ldg(g.L + o + 32));
-            }
-        }
         for (int i = 0; i < nt; ++i) {
             produce();
-            if constexpr (METLDPC_PIPE_LPF > 0 && PC::NL == 0) {
-                // L1 prefetch of the L lines (2 per active slot) of CN i + LPF: lane 2s + h
-                // takes chunk h of slot s; no registers held, the gathers of that CN then hit L1.
-                const int ip = i + METLDPC_PIPE_LPF;
-                if (ip < nt && lane < 2 * NA) {
-                    const float* a = g.L + s_idx[cb * PC::IDX + ip * NA + (lane >> 1)] + (lane & 1) * 32;
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
-                }
-            }
             const uint32_t st = nc % kPipeStages, ph = (nc / kPipeStages) & 1u;
             ++nc;
             const uint32_t swx = __shfl_sync(FULL, sw_l.x, i), swy = __shfl_sync(FULL, sw_l.y, i);
@@ -677,20 +634,7 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND>::THREADS, 1)
 #pragma unroll
             for (int s = 0; s < NA; ++s) {
                 offs[s] = uint32_t(idx[s]) + uint32_t(lane);
-                if constexpr (PC::NL == 0) {
-                    if constexpr (METLDPC_PIPE_LREG) L2[s] = Lnx[s];
-                    else L2[s] = make_float2(__ldg(g.L + offs[s]), __ldg(g.L + offs[s] + 32));
-                }
-            }
-            if constexpr (METLDPC_PIPE_LREG && PC::NL == 0) {
-                if (i + 1 < nt) {
-                    const int* ix = idx + NA;
-#pragma unroll
-                    for (int s = 0; s < NA; ++s) {
-                        const uint32_t o = uint32_t(ix[s]) + uint32_t(lane);
-                        Lnx[s] = make_float2(__ldg(g.L + o), __ldg(g.L + o + 32));
-                    }
-                }
+                L2[s] = make_float2(__ldg(g.L + offs[s]), __ldg(g.L + offs[s] + 32));   // L2-resident gathers
             }
             mbar_wait(bar_a + 8 * st, ph);
             const float* sr = reinterpret_cast<const float*>(stage + st * PC::STG);
@@ -705,8 +649,6 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND>::THREADS, 1)
 #pragma unroll
             for (int s = 0; s < NA; ++s) {
                 r2[s] = make_float2(sr[s * 64 + lane], sr[s * 64 + 32 + lane]);
-                if constexpr (PC::NL > 0)
-                    L2[s] = make_float2(sr[(NA + ND + s) * 64 + lane], sr[(NA + ND + s) * 64 + 32 + lane]);
             }
             float2 lam = make_float2(0.0f, 0.0f);
             if constexpr (ND > 0) lam = make_float2(sr[NA * 64 + lane], sr[NA * 64 + 32 + lane]);
