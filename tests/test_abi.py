@@ -126,3 +126,30 @@ def test_decoder_needs_gpu(lib, code_c1):
     with pytest.raises(B.MetLdpcError) as ei:
         B.Code(code_c1)
     assert ei.value.status == B.EUNSUPPORTED
+
+
+def test_struct_layouts_match_the_header(lib, root, tmp_path):
+    """The ctypes mirrors of metldpc_config_t / metldpc_code_info_t / metldpc_profile_t have
+    the C sizes and field offsets (a gcc probe compiled against include/metldpc.h), and
+    metldpc_config_default fills the documented defaults."""
+    probe = tmp_path / "probe.c"
+    fields = {"metldpc_config_t": [f for f, _ in B.Config._fields_],
+              "metldpc_code_info_t": [f for f, _ in B.CodeInfo._fields_],
+              "metldpc_profile_t": [f for f, _ in B.Profile._fields_]}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "metldpc.h"', "int main(void) {"]
+    for t, fs in fields.items():
+        lines.append(f'printf("{t} %zu\\n", sizeof({t}));')
+        for f in fs:
+            lines.append(f'printf("{t}.{f} %zu\\n", offsetof({t}, {f}));')
+    lines.append("return 0; }")
+    probe.write_text("\n".join(lines))
+    exe = tmp_path / "probe"
+    subprocess.check_call(["gcc", "-std=c11", f"-I{root / 'include'}", str(probe), "-o", str(exe)])
+    got = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True).stdout.splitlines())
+    for t, cls in (("metldpc_config_t", B.Config), ("metldpc_code_info_t", B.CodeInfo), ("metldpc_profile_t", B.Profile)):
+        assert int(got[t]) == C.sizeof(cls), t
+        for f in fields[t]:
+            assert int(got[f"{t}.{f}"]) == getattr(cls, f).offset, (t, f)
+    cfg = B.metldpc_config_default()
+    assert (cfg.rule, cfg.max_iter, cfg.early_term, cfg.lanes_per_group, cfg.groups_in_flight, cfg.lane_refill) == \
+        (B.RULE_EXACT, 100, 1, 64, 2, 1)
