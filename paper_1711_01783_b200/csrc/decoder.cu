@@ -234,6 +234,24 @@ struct GroupJob {
     cudaEvent_t done = nullptr;    // optional: recorded on the group's stream after finalize
 };
 
+// The CN classes of one pass: the small register-only classes first and the pipelined ones
+// last, each launch after the first programmatically dependent on its predecessor, so a
+// class's tail overlaps the next class's start (METLDPC_PDL=0: plain stream order).
+void launch_cn_classes(metldpc_decoder d, const CodeDev& cd, const Group& g, int l, bool check, cudaStream_t s,
+                       const L2Window& w) {
+    static const bool pdl_on = [] {
+        const char* e = std::getenv("METLDPC_PDL");
+        return !(e && e[0] == '0');
+    }();
+    int n = 0;
+    for (int pass = 0; pass < 2; ++pass)
+        for (const auto& c : d->cn_classes) {
+            if (cn_use_pipe(c.D, c.nd) != (pass == 1)) continue;
+            launch_cn(cd, g, d->cfg.rule, c.D, c.nd, c.begin, c.count, c.ts, c.grid, l, check, s, w, pdl_on && n > 0);
+            ++n;
+        }
+}
+
 metldpc_status group_begin(metldpc_decoder d, const GroupJob& j, int N) {
     const CodeDev cd = code_dev(d->code, d->cfg.rule);
     const Group g = group_of(d, j.k);
@@ -254,11 +272,8 @@ void group_iter(metldpc_decoder d, const GroupJob& j, int l) {
     const Group g = group_of(d, j.k);
     const bool et = d->cfg.early_term != 0;
     size_t e = ev_begin(d, 0, j.s);
-    for (const auto& c : d->cn_classes) {
-        launch_cn(cd, g, d->cfg.rule, c.D, c.nd, c.begin, c.count, c.ts, c.grid, l, et && l >= 2, j.s,
-                  d->l2w[size_t(j.k)]);
-        d->prof.launches++;
-    }
+    launch_cn_classes(d, cd, g, l, et && l >= 2, j.s, d->l2w[size_t(j.k)]);
+    d->prof.launches += int64_t(d->cn_classes.size());
     ev_end(d, e, j.s);
     d->prof.cn_launches++;
     d->prof.cn_lane_iters += j.nb;
@@ -310,8 +325,7 @@ metldpc_status loop_graph(metldpc_decoder d, int k, cudaGraphExec_t* out) {
     cudaStream_t cs;
     CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    for (const auto& c : d->cn_classes)
-        launch_cn(cd, g, d->cfg.rule, c.D, c.nd, c.begin, c.count, c.ts, c.grid, 0, et, cs, d->l2w[size_t(k)]);
+    launch_cn_classes(d, cd, g, 0, et, cs, d->l2w[size_t(k)]);
     launch_latch_dev(g, et, cs);
     launch_finish(cd, g, d->vn_grid, cs, d->l2w[size_t(k)]);
     launch_loop_ctl(g, (unsigned long long)h, cs);
@@ -387,8 +401,7 @@ metldpc_status stream_graph(metldpc_decoder d, int k, cudaGraphExec_t* out) {
     // part A: one pass (CN classes, per-lane latch, finish)
     cudaError_t e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
     if (e != cudaSuccess) return fail_capture(e, "stream graph capture: ");
-    for (const auto& c : d->cn_classes)
-        launch_cn(cd, g, d->cfg.rule, c.D, c.nd, c.begin, c.count, c.ts, c.grid, 0, true, cs, d->l2w[size_t(k)]);
+    launch_cn_classes(d, cd, g, 0, true, cs, d->l2w[size_t(k)]);
     launch_latch_stream(g, d->job, (unsigned long long)hi, cs);
     launch_finish(cd, g, d->vn_grid, cs, d->l2w[size_t(k)]);
     cudaGraph_t cap;

@@ -115,6 +115,14 @@ __device__ __forceinline__ void load_phi_table(char* smem, const float* phi) {
 
 // ------------------------------------------------------------------ check-node update (a2 + a4)
 
+// The CN classes of one iteration are independent (disjoint CNs and r rows; the VN sums are
+// order-free integer atomics), so each class launch lets the next one start on SMs it has
+// released (programmatic dependent launch).  Every class kernel waits for its predecessor at
+// its very end, so the finish kernel, a normal launch after the last class, still sees all
+// of them complete.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait_previous() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 struct CnCtl {
     int check;   // test the syndrome of iteration l-1 (reads L^{l-1}, degree-1 bits[rpar])
     int rpar, wpar;
@@ -350,7 +358,11 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
     constexpr int STAGE = (NA <= 4 ? 32 : 8) * NAS;
     extern __shared__ __align__(16) char smem[];
     __shared__ uint32_t s_unsat[2], s_act[2], s_fresh[2];
-    if (*reinterpret_cast<volatile int*>(g.done)) return;
+    pdl_launch_dependents();
+    if (*reinterpret_cast<volatile int*>(g.done)) {
+        pdl_wait_previous();
+        return;
+    }
     const CnCtl k = cn_ctl(karg, g);
     load_phi_table<RULE>(smem, cd.phi);
     if (threadIdx.x < 2) {
@@ -484,6 +496,7 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
     }
     __syncthreads();
     if (k.check && threadIdx.x < 2 && s_unsat[threadIdx.x]) atomicOr(g.unsat + threadIdx.x, s_unsat[threadIdx.x]);
+    pdl_wait_previous();
 }
 
 // ------------------------------------------------------------------ TMA-pipelined CN tiles
@@ -552,7 +565,11 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND>::THREADS, 1)
     constexpr int TS = 32;                     // CNs per tile
     extern __shared__ __align__(16) char smem[];
     __shared__ uint32_t s_unsat[2], s_act[2], s_fresh[2];
-    if (*reinterpret_cast<volatile int*>(g.done)) return;
+    pdl_launch_dependents();
+    if (*reinterpret_cast<volatile int*>(g.done)) {
+        pdl_wait_previous();
+        return;
+    }
     const CnCtl k = cn_ctl(karg, g);
     load_phi_table<RULE>(smem, cd.phi);
     if (threadIdx.x < 2) {
@@ -675,6 +692,7 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND>::THREADS, 1)
     }
     __syncthreads();
     if (k.check && threadIdx.x < 2 && s_unsat[threadIdx.x]) atomicOr(g.unsat + threadIdx.x, s_unsat[threadIdx.x]);
+    pdl_wait_previous();
 }
 
 // Generic class: any lane count, CNs with more than one degree-1 slot or total degree
@@ -685,7 +703,11 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group 
     using PT = PhiT<RULE>;
     extern __shared__ __align__(16) char smem[];
     __shared__ uint32_t s_unsat[4], s_act[4];
-    if (*reinterpret_cast<volatile int*>(g.done)) return;
+    pdl_launch_dependents();
+    if (*reinterpret_cast<volatile int*>(g.done)) {
+        pdl_wait_previous();
+        return;
+    }
     const CnCtl k = cn_ctl(karg, g);
     load_phi_table<RULE>(smem, cd.phi);
     if (threadIdx.x < g.C) { s_unsat[threadIdx.x] = 0u; s_act[threadIdx.x] = g.act[threadIdx.x]; }
@@ -756,6 +778,7 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group 
     }
     __syncthreads();
     if (k.check && threadIdx.x < g.C && s_unsat[threadIdx.x]) atomicOr(g.unsat + threadIdx.x, s_unsat[threadIdx.x]);
+    pdl_wait_previous();
 }
 
 // ------------------------------------------------------------------ syndrome test only (a4 at l = N)
@@ -808,7 +831,7 @@ __global__ void __launch_bounds__(256) k_finish(CodeDev cd, Group g) {
         const float4 lam = __ldg(reinterpret_cast<const float4*>(g.lam_a + size_t(a) * g.B) + q);
         const int b0 = q * 4;
         const uint32_t m = (s_act[b0 >> 5] >> (b0 & 31)) & 0xFu;
-        float4 L = Lrow[q];
+        float4 L = (m == 0xFu) ? make_float4(0.f, 0.f, 0.f, 0.f) : Lrow[q];   // all 4 lanes rewritten: skip the read
         const float sc = 1.0f / 131072.0f;
         if (m & 1u) L.x = __fadd_rn(lam.x, __fmul_rn(__int2float_rn(int(acc.x - bias)), sc));
         if (m & 2u) L.y = __fadd_rn(lam.y, __fmul_rn(__int2float_rn(int(acc.y - bias)), sc));
@@ -1548,28 +1571,35 @@ void launch_loop_ctl(const Group& g, unsigned long long cond_handle, cudaStream_
 // Optional persisting-L2 window over the group's L / accumulator rows (set by the decoder
 // when the device supports it).
 static cudaError_t launch_with_window(void* f, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t s,
-                                      const L2Window& w) {
+                                      const L2Window& w, bool pdl = false) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
+    unsigned na = 0;
     if (w.bytes) {
-        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-        attr[0].val.accessPolicyWindow.base_ptr = w.base;
-        attr[0].val.accessPolicyWindow.num_bytes = w.bytes;
-        attr[0].val.accessPolicyWindow.hitRatio = w.hit_ratio;
-        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[na].val.accessPolicyWindow.base_ptr = w.base;
+        attr[na].val.accessPolicyWindow.num_bytes = w.bytes;
+        attr[na].val.accessPolicyWindow.hitRatio = w.hit_ratio;
+        attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        ++na;
     }
+    if (pdl) {   // programmatic dependent launch: may start while the previous CN class drains
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = na ? attr : nullptr;
+    cfg.numAttrs = na;
     return cudaLaunchKernelExC(&cfg, f, args);
 }
 
 void launch_cn(const CodeDev& cd, const Group& g, int rule, int D, int nd, int begin, int count, int ts, int grid,
-               int l, bool check, cudaStream_t s, const L2Window& w) {
+               int l, bool check, cudaStream_t s, const L2Window& w, bool pdl) {
     CnCtl k{check ? 1 : 0, (l - 1) & 1, l & 1, l == 0 ? 1 : 0, check ? 1 : 0};
     if (cn_use_pipe(D, nd)) {
         void* f = rule == METLDPC_RULE_EXACT ? cn_pipe_kernel<METLDPC_RULE_EXACT>(D - nd, nd)
@@ -1578,16 +1608,16 @@ void launch_cn(const CodeDev& cd, const Group& g, int rule, int D, int nd, int b
         size_t sm;   // the smem attribute was set by cn_blocks_per_sm
         cn_pipe_geom(rule, D, nd, &th, &sm);
         void* args[] = {const_cast<CodeDev*>(&cd), const_cast<Group*>(&g), &k, &begin, &count};
-        launch_with_window(f, dim3(grid), dim3(th), args, sm, s, w);
+        launch_with_window(f, dim3(grid), dim3(th), args, sm, s, w, pdl);
         return;
     }
     void* f = cn_kernel(rule, D, nd);
     if (D < 0) {
         void* args[] = {const_cast<CodeDev*>(&cd), const_cast<Group*>(&g), &k, &begin, &count};
-        launch_with_window(f, dim3(grid), dim3(kCnThreads), args, cn_smem(rule, D, nd), s, w);
+        launch_with_window(f, dim3(grid), dim3(kCnThreads), args, cn_smem(rule, D, nd), s, w, pdl);
     } else {
         void* args[] = {const_cast<CodeDev*>(&cd), const_cast<Group*>(&g), &k, &begin, &count, &ts};
-        launch_with_window(f, dim3(grid), dim3(kCnThreads), args, cn_smem(rule, D, nd), s, w);
+        launch_with_window(f, dim3(grid), dim3(kCnThreads), args, cn_smem(rule, D, nd), s, w, pdl);
     }
 }
 

@@ -96,7 +96,8 @@ void launch_refill_wave(const CodeDev& cd, const Group& g, StreamJob* job, cudaS
 // l >= 1: iteration given by the host; l == 0: read from Group::iter (graph body), with
 // et telling whether iterations >= 2 test the syndrome.
 void launch_cn(const CodeDev& cd, const Group& g, int rule, int D, int nd, int begin, int count, int ts, int grid,
-               int l, bool check, cudaStream_t s, const L2Window& w);
+               int l, bool check, cudaStream_t s, const L2Window& w, bool pdl = false);
+bool cn_use_pipe(int D, int nd);   // class runs the TMA-pipelined kernel
 void launch_finish(const CodeDev& cd, const Group& g, int grid, cudaStream_t s, const L2Window& w);
 void launch_check(const CodeDev& cd, const Group& g, int grid, int l, cudaStream_t s);
 void launch_latch(const Group& g, int l, bool final_, cudaStream_t s);
