@@ -237,12 +237,17 @@ struct GroupJob {
 // The CN classes of one pass: the small register-only classes first and the pipelined ones
 // last, each launch after the first programmatically dependent on its predecessor, so a
 // class's tail overlaps the next class's start (METLDPC_PDL=0: plain stream order).
-void launch_cn_classes(metldpc_decoder d, const CodeDev& cd, const Group& g, int l, bool check, cudaStream_t s,
-                       const L2Window& w) {
-    static const bool pdl_on = [] {
+bool pdl_enabled() {
+    static const bool on = [] {
         const char* e = std::getenv("METLDPC_PDL");
         return !(e && e[0] == '0');
     }();
+    return on;
+}
+
+void launch_cn_classes(metldpc_decoder d, const CodeDev& cd, const Group& g, int l, bool check, cudaStream_t s,
+                       const L2Window& w) {
+    const bool pdl_on = pdl_enabled();
     int n = 0;
     for (int pass = 0; pass < 2; ++pass)
         for (const auto& c : d->cn_classes) {
@@ -326,9 +331,10 @@ metldpc_status loop_graph(metldpc_decoder d, int k, cudaGraphExec_t* out) {
     CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     launch_cn_classes(d, cd, g, 0, et, cs, d->l2w[size_t(k)]);
-    launch_latch_dev(g, et, cs);
-    launch_finish(cd, g, d->vn_grid, cs, d->l2w[size_t(k)]);
-    launch_loop_ctl(g, (unsigned long long)h, cs);
+    const bool pdl = pdl_enabled();
+    launch_latch_dev(g, et, cs, pdl);
+    launch_finish(cd, g, d->vn_grid, cs, d->l2w[size_t(k)], pdl);
+    launch_loop_ctl(g, (unsigned long long)h, cs, pdl);
     cudaGraph_t captured;
     cudaError_t e = cudaStreamEndCapture(cs, &captured);
     cudaStreamDestroy(cs);
@@ -402,8 +408,8 @@ metldpc_status stream_graph(metldpc_decoder d, int k, cudaGraphExec_t* out) {
     cudaError_t e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
     if (e != cudaSuccess) return fail_capture(e, "stream graph capture: ");
     launch_cn_classes(d, cd, g, 0, true, cs, d->l2w[size_t(k)]);
-    launch_latch_stream(g, d->job, (unsigned long long)hi, cs);
-    launch_finish(cd, g, d->vn_grid, cs, d->l2w[size_t(k)]);
+    launch_latch_stream(g, d->job, (unsigned long long)hi, cs, pdl_enabled());
+    launch_finish(cd, g, d->vn_grid, cs, d->l2w[size_t(k)], pdl_enabled());
     cudaGraph_t cap;
     if ((e = cudaStreamEndCapture(cs, &cap)) != cudaSuccess) return fail_capture(e, "stream graph capture: ");
     // the last node of part A (a single-stream capture is a chain: the node without successors)

@@ -816,6 +816,8 @@ __global__ void __launch_bounds__(256) k_check(CodeDev cd, Group g, int par) {
 // and clear the accumulator for the next iteration.  Four lanes per thread (128-bit).
 __global__ void __launch_bounds__(256) k_finish(CodeDev cd, Group g) {
     __shared__ uint32_t s_act[4];
+    pdl_launch_dependents();
+    pdl_wait_previous();   // may be launched ahead of the latch it follows
     if (*reinterpret_cast<volatile int*>(g.done)) return;
     if (threadIdx.x < g.C) s_act[threadIdx.x] = g.act[threadIdx.x];
     __syncthreads();
@@ -922,6 +924,8 @@ __global__ void k_latch(Group g, int l, int final_) {
 // Graph-loop versions: latch the lanes converged at l - 1 after CN pass l (ET), and
 // advance l, leaving the WHILE condition = (l <= N && some lane still iterating).
 __global__ void k_latch_dev(Group g, int et) {
+    pdl_launch_dependents();
+    pdl_wait_previous();   // launched programmatically after the CN classes: their results first
     const int l = *reinterpret_cast<volatile int*>(g.iter);
     if (!et || l < 2) return;
     const int c = threadIdx.x;
@@ -946,6 +950,7 @@ __global__ void k_latch_dev(Group g, int et) {
 }
 
 __global__ void k_loop_ctl(Group g, cudaGraphConditionalHandle h) {
+    pdl_wait_previous();
     const int l = *g.iter + 1;
     *g.iter = l;
     cudaGraphSetConditional(h, (l <= *g.maxit && !*reinterpret_cast<volatile int*>(g.done)) ? 1u : 0u);
@@ -1105,6 +1110,8 @@ __global__ void k_stream_init(Group g) {
 // Requests a refill wave (IF node) once wave_min lanes wait or no lane iterates.
 __global__ void k_latch_stream(Group g, StreamJob* job, cudaGraphConditionalHandle if_h) {
     __shared__ uint32_t s_act[4], s_fin[4];
+    pdl_launch_dependents();
+    pdl_wait_previous();
     const int b = threadIdx.x, c = b >> 5, bit = b & 31;
     const int l = *reinterpret_cast<volatile int*>(g.iter);
     const int N = job->N;
@@ -1543,12 +1550,33 @@ void launch_pack_syndrome(const CodeDev& cd, const Group& g, const uint32_t* syn
 
 void launch_init_ctl(const Group& g, int nb, int N, cudaStream_t s) { k_init_ctl<<<1, 128, 0, s>>>(g, nb, N); }
 
-void launch_latch_dev(const Group& g, bool et, cudaStream_t s) { k_latch_dev<<<1, 32, 0, s>>>(g, et ? 1 : 0); }
+static void launch_small(void* f, dim3 grid, dim3 block, void** args, cudaStream_t s, bool pdl) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    if (pdl) {
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    cudaLaunchKernelExC(&cfg, f, args);
+}
+
+void launch_latch_dev(const Group& g, bool et, cudaStream_t s, bool pdl) {
+    int e = et ? 1 : 0;
+    void* args[] = {const_cast<Group*>(&g), &e};
+    launch_small(reinterpret_cast<void*>(&k_latch_dev), dim3(1), dim3(32), args, s, pdl);
+}
 
 void launch_stream_init(const Group& g, cudaStream_t s) { k_stream_init<<<1, 128, 0, s>>>(g); }
 
-void launch_latch_stream(const Group& g, StreamJob* job, unsigned long long if_handle, cudaStream_t s) {
-    k_latch_stream<<<1, 128, 0, s>>>(g, job, cudaGraphConditionalHandle(if_handle));
+void launch_latch_stream(const Group& g, StreamJob* job, unsigned long long if_handle, cudaStream_t s, bool pdl) {
+    cudaGraphConditionalHandle h = cudaGraphConditionalHandle(if_handle);
+    void* args[] = {const_cast<Group*>(&g), &job, &h};
+    launch_small(reinterpret_cast<void*>(&k_latch_stream), dim3(1), dim3(128), args, s, pdl);
 }
 
 void launch_stream_ctl(const Group& g, unsigned long long while_handle, cudaStream_t s) {
@@ -1564,8 +1592,10 @@ void launch_refill_wave(const CodeDev& cd, const Group& g, StreamJob* job, cudaS
     k_refill_activate<<<1, 128, 0, s>>>(g);
 }
 
-void launch_loop_ctl(const Group& g, unsigned long long cond_handle, cudaStream_t s) {
-    k_loop_ctl<<<1, 1, 0, s>>>(g, cudaGraphConditionalHandle(cond_handle));
+void launch_loop_ctl(const Group& g, unsigned long long cond_handle, cudaStream_t s, bool pdl) {
+    cudaGraphConditionalHandle h = cudaGraphConditionalHandle(cond_handle);
+    void* args[] = {const_cast<Group*>(&g), &h};
+    launch_small(reinterpret_cast<void*>(&k_loop_ctl), dim3(1), dim3(1), args, s, pdl);
 }
 
 // Optional persisting-L2 window over the group's L / accumulator rows (set by the decoder
@@ -1621,9 +1651,9 @@ void launch_cn(const CodeDev& cd, const Group& g, int rule, int D, int nd, int b
     }
 }
 
-void launch_finish(const CodeDev& cd, const Group& g, int grid, cudaStream_t s, const L2Window& w) {
+void launch_finish(const CodeDev& cd, const Group& g, int grid, cudaStream_t s, const L2Window& w, bool pdl) {
     void* args[] = {const_cast<CodeDev*>(&cd), const_cast<Group*>(&g)};
-    launch_with_window(reinterpret_cast<void*>(&k_finish), dim3(grid), dim3(256), args, 0, s, w);
+    launch_with_window(reinterpret_cast<void*>(&k_finish), dim3(grid), dim3(256), args, 0, s, w, pdl);
 }
 
 void launch_check(const CodeDev& cd, const Group& g, int grid, int l, cudaStream_t s) {

@@ -86,11 +86,12 @@ void launch_scatter(const CodeDev& cd, const Group& g, const float* llr, int nb,
 void launch_pack_syndrome(const CodeDev& cd, const Group& g, const uint32_t* synd, int nb, cudaStream_t s);
 void launch_init_ctl(const Group& g, int nb, int N, cudaStream_t s);
 // Device-driven iteration control for the CUDA-graph loop (l read from Group::iter).
-void launch_latch_dev(const Group& g, bool et, cudaStream_t s);
-void launch_loop_ctl(const Group& g, unsigned long long cond_handle, cudaStream_t s);
+void launch_latch_dev(const Group& g, bool et, cudaStream_t s, bool pdl = false);
+void launch_loop_ctl(const Group& g, unsigned long long cond_handle, cudaStream_t s, bool pdl = false);
 // lane refill (streaming decode)
 void launch_stream_init(const Group& g, cudaStream_t s);
-void launch_latch_stream(const Group& g, StreamJob* job, unsigned long long if_handle, cudaStream_t s);
+void launch_latch_stream(const Group& g, StreamJob* job, unsigned long long if_handle, cudaStream_t s,
+                         bool pdl = false);
 void launch_stream_ctl(const Group& g, unsigned long long while_handle, cudaStream_t s);
 void launch_refill_wave(const CodeDev& cd, const Group& g, StreamJob* job, cudaStream_t s);
 // l >= 1: iteration given by the host; l == 0: read from Group::iter (graph body), with
@@ -98,7 +99,7 @@ void launch_refill_wave(const CodeDev& cd, const Group& g, StreamJob* job, cudaS
 void launch_cn(const CodeDev& cd, const Group& g, int rule, int D, int nd, int begin, int count, int ts, int grid,
                int l, bool check, cudaStream_t s, const L2Window& w, bool pdl = false);
 bool cn_use_pipe(int D, int nd);   // class runs the TMA-pipelined kernel
-void launch_finish(const CodeDev& cd, const Group& g, int grid, cudaStream_t s, const L2Window& w);
+void launch_finish(const CodeDev& cd, const Group& g, int grid, cudaStream_t s, const L2Window& w, bool pdl = false);
 void launch_check(const CodeDev& cd, const Group& g, int grid, int l, cudaStream_t s);
 void launch_latch(const Group& g, int l, bool final_, cudaStream_t s);
 void launch_finalize(const CodeDev& cd, const Group& g, int nb, uint32_t* bits_out, int32_t* iters_out,
