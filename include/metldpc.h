@@ -61,8 +61,11 @@ typedef struct {
     int32_t lanes_per_group;   /* codewords interleaved per group: 32, 64 or 128; default 64
                                   (coalesced when a multiple of 32)               */
     int32_t groups_in_flight;  /* lane groups decoded concurrently on their own streams, 1..8;
-                                  default 2 (each has its own ~1 GB workspace at C3; their
-                                  kernels fill each other's ramps, tails and launch gaps)   */
+                                  default 1 (each has its own ~1 GB workspace at C3).  With 1
+                                  the decoder keeps its posterior / VN-sum rows in a persisting
+                                  L2 window (it sets the context's
+                                  cudaLimitPersistingL2CacheSize; METLDPC_L2PERSIST=0
+                                  disables)                                                   */
     int32_t lane_refill;       /* 1 = streaming decode (needs early_term, 64-lane groups): a lane
                                   whose frame has latched takes the next frame of the batch in
                                   a refill wave while the other lanes keep iterating, so a

@@ -152,4 +152,4 @@ def test_struct_layouts_match_the_header(lib, root, tmp_path):
             assert int(got[f"{t}.{f}"]) == getattr(cls, f).offset, (t, f)
     cfg = B.metldpc_config_default()
     assert (cfg.rule, cfg.max_iter, cfg.early_term, cfg.lanes_per_group, cfg.groups_in_flight, cfg.lane_refill) == \
-        (B.RULE_EXACT, 100, 1, 64, 2, 1)
+        (B.RULE_EXACT, 100, 1, 64, 1, 1)

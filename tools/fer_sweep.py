@@ -31,7 +31,7 @@ def main():
     ap.add_argument("--rule", choices=["exact", "lut"], default="exact")
     ap.add_argument("--key", type=int, default=5)
     ap.add_argument("--out", default=None)
-    ap.add_argument("--groups", type=int, default=2, help="lane groups in flight")
+    ap.add_argument("--groups", type=int, default=1, help="lane groups in flight")
     ap.add_argument("--no-refill", action="store_true", help="group mode instead of lane refill")
     a = ap.parse_args()
 
