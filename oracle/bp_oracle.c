@@ -28,7 +28,8 @@
  *       fold in the caller's CSC slot order; in fp32 (M3) an exact fixed-point sum
  *       with 2^-17 resolution (N3, see vn_phase32).
  *   Decisions (Step 5, Eq. 5): c_i = [L_i < 0] for active VNs,
- *       c_v = [lambda_v + rho_v < 0] for degree-1 VNs (rho = their CN output);
+ *       c_v = [lambda_v + rho_v < 0] for degree-1 VNs (rho = their CN output; in
+ *       fp32 (M3) the unclamped rho, compared in the phi domain: DESIGN.md N1);
  *       a tie (exact zero) gives 0 -- "if q_i^l > 1, c_i = 1".
  *   Syndrome test (Step 5): stop at the first l with H c^T = S_B when early
  *       termination is on; otherwise run N iterations and test once.
@@ -255,7 +256,7 @@ void orc_syndrome(int n, int m, const int64_t* cn_ptr, const int32_t* edge_vn,
 
 /* ---- fp32 (M3) ---- */
 static void cn_phase32(const graph_t* g, int rule, const float* lam, const uint32_t* synd,
-                       const float* r_old, const float* L_old, float* r_new, float* rho /*[n]*/) {
+                       const float* r_old, const float* L_old, float* r_new, uint8_t* dec1 /*[n]*/) {
     int D = g->max_cdeg;
     float* x = malloc(sizeof(float) * (size_t)D);
     float* p = malloc(sizeof(float) * (size_t)D);
@@ -285,12 +286,20 @@ static void cn_phase32(const graph_t* g, int rule, const float* lam, const uint3
         for (int k = d - 2; k >= 0; --k) Q[k] = Q[k + 1] + p[k + 1];
         for (int k = 0; k < d; ++k) {
             float S = P[k] + Q[k];
-            float mag = fminf(orc_phi32(rule, S), (float)R_MAX);
             int neg = par ^ (x[k] < 0.0f);
-            float o = neg ? -mag : mag;
             int64_t e = slot_e[k];
-            if (g->act_id[e] >= 0) r_new[g->act_id[e]] = o;
-            else rho[g->edge_vn[e]] = o;
+            if (g->act_id[e] >= 0) {
+                float mag = fminf(orc_phi32(rule, S), (float)R_MAX);
+                r_new[g->act_id[e]] = neg ? -mag : mag;
+            } else {
+                /* Step 5 for the degree-1 VN v (N1): c_v = [lambda_v + rho_v < 0]
+                 * for the unclamped CN output rho_v = (-1)^neg phi(S_k).  Since
+                 * |rho_v| = phi(S_k), |lambda_v| = phi(p_k) and phi is decreasing,
+                 * |rho_v| > |lambda_v| <=> S_k < p_k: equal signs decide by that sign,
+                 * opposite signs by the larger magnitude, an exact tie gives 0. */
+                int nl = x[k] < 0.0f;
+                dec1[g->edge_vn[e]] = nl ? (uint8_t)(neg || p[k] < S) : (uint8_t)(neg && S < p[k]);
+            }
         }
     }
     free(x); free(p); free(P); free(Q); free(slot_e);
@@ -315,9 +324,9 @@ static void vn_phase32(const graph_t* g, const float* lam, const float* r_new, f
     }
 }
 
-static void decide32(const graph_t* g, const float* lam, const float* L, const float* rho, uint8_t* c) {
+static void decide32(const graph_t* g, const float* L, const uint8_t* dec1, uint8_t* c) {
     for (int v = 0; v < g->n; ++v)
-        c[v] = (g->vn_act[v] >= 0) ? (L[g->vn_act[v]] < 0.0f) : ((lam[v] + rho[v]) < 0.0f);
+        c[v] = (g->vn_act[v] >= 0) ? (L[g->vn_act[v]] < 0.0f) : dec1[v];
 }
 
 static int all_finite32(const float* a, int n) {
@@ -342,13 +351,13 @@ int orc_decode_f32(int rule, int n, int m, const int64_t* cn_ptr, const int32_t*
     size_t Ea = (size_t)(g.E_it > 0 ? g.E_it : 1), Na = (size_t)(g.n_a > 0 ? g.n_a : 1);
     float* r_old = calloc(Ea, 4); float* r_new = calloc(Ea, 4);
     float* L_old = malloc(Na * 4); float* L_new = malloc(Na * 4);
-    float* rho = calloc((size_t)n, 4);
+    uint8_t* dec1 = calloc((size_t)n, 1);
     for (int a = 0; a < g.n_a; ++a) L_old[a] = lam[g.act_vn[a]];   /* Step 2: L^0 = lambda, r^0 = 0 */
     int it = 0, conv = 0;
     for (int l = 1; l <= max_iter; ++l) {
-        cn_phase32(&g, rule, lam, synd, r_old, L_old, r_new, rho);
+        cn_phase32(&g, rule, lam, synd, r_old, L_old, r_new, dec1);
         vn_phase32(&g, lam, r_new, L_new);
-        decide32(&g, lam, L_new, rho, bits_out);
+        decide32(&g, L_new, dec1, bits_out);
         if (r_trace) memcpy(r_trace + (size_t)(l - 1) * g.E_it, r_new, (size_t)g.E_it * 4);
         if (L_trace) memcpy(L_trace + (size_t)(l - 1) * g.n_a, L_new, (size_t)g.n_a * 4);
         float* t;
@@ -360,7 +369,7 @@ int orc_decode_f32(int rule, int n, int m, const int64_t* cn_ptr, const int32_t*
     if (!early_term || !conv) conv = syndrome_matches(&g, bits_out, synd);
     *iters_out = it;
     *conv_out = (uint8_t)conv;
-    free(r_old); free(r_new); free(L_old); free(L_new); free(rho);
+    free(r_old); free(r_new); free(L_old); free(L_new); free(dec1);
     graph_free(&g);
     return 0;
 }
@@ -394,9 +403,12 @@ static void cn_phase64(const graph_t* g, int rule, const double* lam, const uint
         Q[d - 1] = 0.0;
         for (int k = d - 2; k >= 0; --k) Q[k] = Q[k + 1] + p[k + 1];
         for (int k = 0; k < d; ++k) {
-            double mag = fmin(orc_phi64(rule, P[k] + Q[k]), R_MAX);
-            double o = (par ^ (x[k] < 0.0)) ? -mag : mag;
             int64_t e = slot_e[k];
+            /* R_MAX clamps the stored messages only (R6); a degree-1 VN's CN output is not
+             * stored, its decision takes the unclamped posterior lambda + rho (N1) */
+            double mag = orc_phi64(rule, P[k] + Q[k]);
+            if (g->act_id[e] >= 0) mag = fmin(mag, R_MAX);
+            double o = (par ^ (x[k] < 0.0)) ? -mag : mag;
             if (g->act_id[e] >= 0) r_new[g->act_id[e]] = o;
             else rho[g->edge_vn[e]] = o;
         }

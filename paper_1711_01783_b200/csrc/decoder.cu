@@ -123,6 +123,7 @@ CodeDev code_dev(const metldpc_code c, int rule) {
     cd.cn_new = c->d_cn_new;
     cd.phi = (rule == METLDPC_RULE_EXACT) ? c->d_phi_exact : c->d_phi_lut;
     cd.phi_top = phi_top();
+    cd.rule = rule;
     return cd;
 }
 

@@ -106,6 +106,32 @@ __device__ __forceinline__ uint32_t phi_tab_lane(const char* smem, int lane) {
     return r;
 }
 
+// phi(y) of the selected rule read from copy 0 of the device table in global memory -- the
+// same N2 formula as phi_dev, for the once-per-frame users (the degree-1 priors of k_scatter).
+template <int RULE>
+__device__ __forceinline__ float phi_gmem_rule(const float* tab, float y) {
+    using P = PhiT<RULE>;
+    constexpr uint32_t LOW = (1u << (23 - P::J)) - 1u;
+    const uint32_t u = phi_clamp_bits(y);
+    const char* e = reinterpret_cast<const char*>(tab) + size_t((u >> (23 - P::J)) - (kPhiLoBits >> (23 - P::J))) * P::STRIDE;
+    const float ts = __fsub_rn(__uint_as_float((u & LOW) | 0x3F800000u), 1.0f);
+    if constexpr (RULE == METLDPC_RULE_EXACT) {
+        const float4 c = __ldg(reinterpret_cast<const float4*>(e));
+        return __fmaf_rn(__fmaf_rn(__fmaf_rn(c.w, ts, c.z), ts, c.y), ts, c.x);
+    } else {
+        const float2 c = __ldg(reinterpret_cast<const float2*>(e));
+        return __fmaf_rn(c.y, ts, c.x);
+    }
+}
+
+// Degree-1 prior as the CN kernels read it (N1): phi(|lambda|) with the sign bit
+// [lambda < 0] (an input of -0 carries no sign, R2).
+__device__ __forceinline__ float lam1_phi_form(const CodeDev& cd, float lam) {
+    const float ph = (cd.rule == METLDPC_RULE_EXACT) ? phi_gmem_rule<METLDPC_RULE_EXACT>(cd.phi, fabsf(lam))
+                                                     : phi_gmem_rule<METLDPC_RULE_PHI_LUT>(cd.phi, fabsf(lam));
+    return __uint_as_float(__float_as_uint(ph) | (lam < 0.0f ? 0x80000000u : 0u));
+}
+
 template <int RULE>
 __device__ __forceinline__ void load_phi_table(char* smem, const float* phi) {
     using P = PhiT<RULE>;
@@ -154,6 +180,17 @@ __device__ __forceinline__ uint32_t vn_fix(float o) {
     return __float_as_uint(__fmaf_rn(o, 131072.0f, 12582912.0f));
 }
 
+// Degree-1 decision (Step 5; N1): bit = [lambda + rho < 0] for the
+// unclamped posterior, with |rho| = phi(S) and |lambda| = phi(p), p = phi(|lambda|) the
+// stored prior.  phi is a decreasing involution, so |rho| > |lambda| <=> S < p and the
+// decision needs no phi(S): equal signs give that sign, opposite signs the sign of the
+// larger magnitude, an exact tie 0.  nl / nr: sign bits (bit 31) of lambda and rho.
+__device__ __forceinline__ uint32_t d1_decision(uint32_t nl, uint32_t nr, float p, float S) {
+    nl >>= 31;
+    nr >>= 31;
+    return nl ? (nr | uint32_t(p < S)) : (nr & uint32_t(S < p));
+}
+
 template <int RULE, int NA, int ND>
 __device__ __forceinline__ uint32_t cn_lane(uint32_t tabk, const float (&Lv)[NA > 0 ? NA : 1],
                                             const float (&ro)[NA > 0 ? NA : 1], float lam, uint32_t sbit,
@@ -173,10 +210,10 @@ __device__ __forceinline__ uint32_t cn_lane(uint32_t tabk, const float (&Lv)[NA 
         par ^= xb[s];
         p[s] = phi_dev<RULE>(tabk, fabsf(x), one);
     }
-    if constexpr (ND > 0) {                               // degree-1 VN sends its prior
-        xb[NA] = __float_as_uint(__fadd_rn(lam, 0.0f));
+    if constexpr (ND > 0) {          // degree-1 VN sends its prior, stored in phi form (N1)
+        xb[NA] = __float_as_uint(lam);                    // sign bit = [lambda < 0]
         par ^= xb[NA];
-        p[NA] = phi_dev<RULE>(tabk, fabsf(lam), one);
+        p[NA] = fabsf(lam);                               // phi(|lambda|)
     }
     // P_0 = 0, P_{k+1} = P_k + p_k; Q_{D-1} = 0, Q_k = Q_{k+1} + p_{k+1}; S_k = P_k + Q_k.
     // The additions with an exact +0 operand are skipped: p, P, Q >= +0, so 0 + v = v.
@@ -188,16 +225,19 @@ __device__ __forceinline__ uint32_t cn_lane(uint32_t tabk, const float (&Lv)[NA 
 #pragma unroll
     for (int s = D - 1; s >= 0; --s) {
         const float S = (s == D - 1) ? P[s] : (s == 0 ? Q : __fadd_rn(P[s], Q));
+        if (s >= NA) {   // Step 5 for the degree-1 VN: sign of lambda + rho, decided as N1 (no phi(S))
+            d1bit = d1_decision(xb[s], par ^ xb[s], p[s], S);
+            if (s > 0) Q = __fadd_rn(Q, p[s]);
+            continue;
+        }
         const float mag = fminf(phi_dev<RULE>(tabk, S, one), kRMax);
         const float o = __uint_as_float(__float_as_uint(mag) | ((par ^ xb[s]) & 0x80000000u));
-        if (s < NA) {
+        {
             (void)act;   // unpredicated, as in cn_pair
             __stcs(pr + s * 64, o);
             // VN sum (Eq. 4); row offsets from registers for small NA, from shared memory otherwise
             const uint32_t ro_s = (NA <= 4) ? offs[s] : uint32_t(idx[s]);
             atomicAdd(reinterpret_cast<unsigned int*>(pla + ro_s + 64), vn_fix(o));
-        } else {
-            d1bit = uint32_t(__fadd_rn(lam, o) < 0.0f);   // Step 5 for VN_b
         }
         if (s > 0) Q = __fadd_rn(Q, p[s]);
     }
@@ -291,13 +331,12 @@ __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 
         par1 ^= xb1[s];
         p[s] = phi_pair<RULE>(tabk, fabsf(x.x), fabsf(x.y), one);
     }
-    if constexpr (ND > 0) {
-        const float2 lz = f2add(lam, zero2);
-        xb0[NA] = __float_as_uint(lz.x);
-        xb1[NA] = __float_as_uint(lz.y);
+    if constexpr (ND > 0) {          // degree-1 prior in phi form (N1): sign = [lambda < 0], |.| = phi(|lambda|)
+        xb0[NA] = __float_as_uint(lam.x);
+        xb1[NA] = __float_as_uint(lam.y);
         par0 ^= xb0[NA];
         par1 ^= xb1[NA];
-        p[NA] = phi_pair<RULE>(tabk, fabsf(lam.x), fabsf(lam.y), one);
+        p[NA] = make_float2(fabsf(lam.x), fabsf(lam.y));
     }
     P[0] = zero2;
     if constexpr (D > 1) P[1] = p[0];
@@ -307,6 +346,12 @@ __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 
 #pragma unroll
     for (int s = D - 1; s >= 0; --s) {
         const float2 S = (s == D - 1) ? P[s] : (s == 0 ? Q : f2add(P[s], Q));
+        if (s >= NA) {   // Step 5 for the degree-1 VN (N1): no phi(S) needed
+            d1bit = make_uint2(d1_decision(xb0[s], par0 ^ xb0[s], p[s].x, S.x),
+                               d1_decision(xb1[s], par1 ^ xb1[s], p[s].y, S.y));
+            if (s > 0) Q = f2add(Q, p[s]);
+            continue;
+        }
         const float2 ph = phi_pair<RULE>(tabk, S.x, S.y, one);
         const float2 o = make_float2(
             __uint_as_float(__float_as_uint(fminf(ph.x, kRMax)) | ((par0 ^ xb0[s]) & 0x80000000u)),
@@ -321,9 +366,6 @@ __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 
             atomicAdd(pa, __float_as_uint(fx.x));              // VN sum (Eq. 4, N3)
             __stcs(pr + s * 64 + 32, o.y);
             atomicAdd(pa + 32, __float_as_uint(fx.y));
-        } else {
-            const float2 dd = f2add(lam, o);
-            d1bit = make_uint2(uint32_t(dd.x < 0.0f), uint32_t(dd.y < 0.0f));   // Step 5 for VN_b
         }
         if (s > 0) Q = f2add(Q, p[s]);
     }
@@ -728,7 +770,7 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group 
         const uint32_t sbit = (__ldg(g.synd_t + size_t(j) * g.C + c) >> lane) & 1u;
         const int idx = (lane < na) ? __ldg(cd.a_vn + ab + lane) : 0;
         const uint32_t one = one_bits();
-        float p[kMaxCnDeg], P[kMaxCnDeg], xs[kMaxCnDeg];
+        float p[kMaxCnDeg], P[kMaxCnDeg];
         uint32_t negmask = 0, chk = sbit;
         for (int s = 0; s < d; ++s) {
             float x;
@@ -743,9 +785,13 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group 
                 x = __ldcs(g.lam1 + size_t(q) * g.B + off);
                 if (k.check) chk ^= (__ldg(g.d1bits + (size_t(k.rpar) * cd.n_1 + q) * g.C + c) >> lane) & 1u;
             }
-            xs[s] = x;
-            negmask |= (__float_as_uint(__fadd_rn(x, 0.0f)) >> 31) << s;   // = [x < 0]
-            p[s] = phi_dev<RULE>(tabk, fabsf(x), one);
+            if (s < na) {
+                negmask |= (__float_as_uint(__fadd_rn(x, 0.0f)) >> 31) << s;   // = [x < 0]
+                p[s] = phi_dev<RULE>(tabk, fabsf(x), one);
+            } else {   // degree-1 prior in phi form (N1): sign bit = [lambda < 0], |x| = phi(|lambda|)
+                negmask |= (__float_as_uint(x) >> 31) << s;
+                p[s] = fabsf(x);
+            }
         }
         if (k.check) {
             const uint32_t mm = __ballot_sync(FULL, chk) & amask;
@@ -758,19 +804,23 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group 
         float Q = 0.0f;
         for (int s = d - 1; s >= 0; --s) {
             const float S = __fadd_rn(P[s], Q);
+            if (s >= na) {   // Step 5 for a degree-1 VN (N1): no phi(S) needed
+                const uint32_t nl = (negmask >> s) & 1u, nr = par ^ nl;
+                const uint32_t bal = __ballot_sync(FULL, d1_decision(nl << 31, nr << 31, p[s], S));
+                if (lane == 0) {
+                    uint32_t* w = g.d1bits + (size_t(k.wpar) * cd.n_1 + db + (s - na)) * g.C + c;
+                    *w = (amask == FULL) ? bal : ((bal & amask) | (*w & ~amask));
+                }
+                if (s > 0) Q = __fadd_rn(Q, p[s]);
+                continue;
+            }
             const float mag = fminf(phi_dev<RULE>(tabk, S, one), kRMax);
             const float o = __uint_as_float(__float_as_uint(mag) | ((par ^ ((negmask >> s) & 1u)) << 31));
-            if (s < na) {
+            {
                 const int v = __shfl_sync(FULL, idx, s);      // whole warp: lane s may be an idle lane
                 if (act) {
                     __stcs(g.r + size_t(ab + s) * g.B + off, o);
                     atomicAdd(reinterpret_cast<unsigned int*>(g.L + size_t(v) * 2 * g.B + g.B + off), vn_fix(o));
-                }
-            } else {
-                const uint32_t bal = __ballot_sync(FULL, __fadd_rn(xs[s], o) < 0.0f);
-                if (lane == 0) {
-                    uint32_t* w = g.d1bits + (size_t(k.wpar) * cd.n_1 + db + (s - na)) * g.C + c;
-                    *w = (amask == FULL) ? bal : ((bal & amask) | (*w & ~amask));
                 }
             }
             if (s > 0) Q = __fadd_rn(Q, p[s]);
@@ -983,7 +1033,7 @@ __global__ void __launch_bounds__(256) k_scatter(CodeDev cd, Group g, const floa
             g.L[size_t(v) * 2 * g.B + off] = val;                    // L^0 = lambda (Step 2)
             g.L[size_t(v) * 2 * g.B + g.B + off] = 0.0f;             // empty VN-sum accumulator
         } else {
-            g.lam1[size_t(~v) * g.B + off] = val;
+            g.lam1[size_t(~v) * g.B + off] = lam1_phi_form(cd, val);
         }
     }
 }
@@ -1261,7 +1311,7 @@ __global__ void __launch_bounds__(256) k_refill_scatter(CodeDev cd, Group g, Str
             g.L[size_t(v) * 2 * g.B + off] = val;
             g.L[size_t(v) * 2 * g.B + g.B + off] = 0.0f;
         } else {
-            g.lam1[size_t(~v) * g.B + off] = val;
+            g.lam1[size_t(~v) * g.B + off] = lam1_phi_form(cd, val);
         }
     }
 }

@@ -17,7 +17,8 @@ struct Group {
     float* L;          // [n_a][2][B] row of VN a: posterior LLR L (Eq. 5) at +0, the fixed-point
                        //             accumulator of the next L (uint32, N3) at +B
     float* lam_a;      // [n_a][B]    channel LLR of active VNs (Eq. 1)
-    float* lam1;       // [n_1][B]    channel LLR of degree-1 VNs, CSR slot order
+    float* lam1;       // [n_1][B]    degree-1 priors in phi form: phi(|lambda|), sign bit [lambda < 0]
+                       //             (N1), CSR slot order
     uint32_t* d1bits;  // [2][n_1][C] hard bits of degree-1 VNs, by iteration parity
     uint32_t* synd_t;  // [m][C]      S_B bits, lane-transposed
     uint32_t* act;     // [C]  lanes still iterating
@@ -64,6 +65,7 @@ struct CodeDev {
     const int32_t* cn_new;  // original CN id -> relabelled id
     const float* phi;      // table of the selected rule
     float phi_top;
+    int rule;              // METLDPC_RULE_EXACT / METLDPC_RULE_PHI_LUT
 };
 
 // returns the number of CTAs per SM the CN kernel reaches (for persistent grids)

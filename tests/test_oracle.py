@@ -375,3 +375,52 @@ def test_md_product_table_and_alice_llr(d):
     lam0 = bp.md_alice_f32(x.astype(np.float32), alpha0.astype(np.float32), snr, d).astype(np.float64)
     xn0 = np.repeat(np.linalg.norm(x.reshape(-1, d), axis=1), d)
     assert np.allclose(lam0, 2 * math.sqrt(snr * (1 + snr)) * xn0 * (1 - 2.0 * u) / math.sqrt(d), rtol=1e-5, atol=1e-5)
+
+
+# ----------------------------------------------------------------- degree-1 decision (N1)
+
+def _two_check_code():
+    """VNs 0-2 of degree 2 on CN 0 and CN 1 (active), VN 3 degree-1 on CN 0, VN 4 on CN 1."""
+    h = np.array([[1, 1, 1, 1, 0],
+                  [1, 1, 1, 0, 1]], np.uint8)
+    return from_dense(h)
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+@pytest.mark.parametrize("rule", [bp.RULE_EXACT, bp.RULE_PHI_LUT])
+def test_degree1_decision_is_posterior_sign(prec, rule):
+    """Step 5 ("c_i = 1 if q_i > 1") for a degree-1 VN after one iteration: its
+    posterior ratio is q^0 times the CN ratio (Eq. 5 with one factor), i.e. the LLR
+    lambda_d + 2 atanh(sigma prod tanh(lambda_a / 2)) -- the closed form of Eqs. (2)-(3),
+    evaluated here in fp64 without phi.  Away from ties every precision and rule must give
+    its sign, including the fp32 replay's phi-domain comparison (S_k < p_k)."""
+    code = _two_check_code()
+    rng = np.random.default_rng(7)
+    checked = 0
+    for t in range(400):
+        lam = rng.normal(0.0, 3.0, 5) * rng.choice([0.05, 1.0, 4.0], 5)
+        s0 = int(rng.integers(0, 2))
+        t_prod = np.prod(np.tanh(lam[:3] / 2.0)) * (1 - 2 * s0)
+        rho = 2.0 * np.arctanh(np.clip(t_prod, -1 + 1e-16, 1 - 1e-16))
+        post = lam[3] + rho
+        if abs(rho) > 25 or abs(post) < 0.05 * max(1.0, abs(lam[3])):
+            continue   # fp32 saturation / near-tie: the sign is not fixed by the closed form
+        o = bp.decode(code, lam, pack_bits([s0, 0]), 1, early_term=False, rule=rule, prec=prec)
+        assert int(o["bits"][3]) == int(post < 0), (t, lam, s0)
+        checked += 1
+    assert checked > 200
+
+
+def test_degree1_decision_unclamped():
+    """R6 clamps stored messages only: a degree-1 VN with lambda = -30.5 whose CN output is
+    about +30.9 (three inputs of 32: rho = 2 atanh(tanh(16)^3) = 30.9) has a positive
+    posterior -> bit 0, although the clamped message 30 would give -0.5 -> bit 1."""
+    code = _two_check_code()
+    lam = np.array([32.0, 32.0, 32.0, -30.5, 1.0])
+    # tanh(16) rounds to 1 in double, so take the phi form of the same closed form
+    rho = bp.phi_def(3 * bp.phi_def(32.0))
+    assert 30.5 < rho < 31.0
+    for prec in (32, 64):
+        for rule in (bp.RULE_EXACT, bp.RULE_PHI_LUT):
+            o = bp.decode(code, lam, pack_bits([0, 0]), 1, early_term=False, rule=rule, prec=prec)
+            assert int(o["bits"][3]) == 0, (prec, rule)
