@@ -223,7 +223,8 @@ std::vector<float> phi_device_table(int rule) {
     // coefficients pre-scaled by 2^(J q) (exact: power-of-two scaling of an fp32 value), so the
     // kernel evaluates the polynomial in t / 2^J -- bit-identical results (kernels.cu phi_dev)
     const int J = ex ? kPhiJExact : kPhiJLut;
-    std::vector<float> dev(size_t(nb + 1) * kPhiCopies * per, 0.0f);   // last bin: zero sentinel
+    const int zb = ex ? kPhiZeroBinsExact : kPhiZeroBinsLut;            // zero bins for [2^6, 2^7)
+    std::vector<float> dev(size_t(nb + zb) * kPhiCopies * per, 0.0f);
     for (int b = 0; b < nb; ++b)
         for (int k = 0; k < kPhiCopies; ++k)
             for (int q = 0; q < per; ++q)

@@ -18,6 +18,10 @@ constexpr int kPhiBinsExact = (kPhiEHi - kPhiELo) << kPhiJExact;   // 800
 constexpr int kPhiBinsLut = (kPhiEHi - kPhiELo) << kPhiJLut;       // 1600
 constexpr uint32_t kPhiLoBits = uint32_t(127 + kPhiELo) << 23;     // 2^-44
 constexpr uint32_t kPhiHiBits = uint32_t(127 + kPhiEHi) << 23;     // 2^6
+// The device copy appends one binade of all-zero bins, [2^6, 2^7): phi = 0 there as above, so
+// a sum S < 2^7 (every S of a check of total degree <= 5: S <= 4 phi(2^-44) = 124.8) needs no
+// upper clamp (kernels.cu phi_pair<RULE, false>).
+constexpr int kPhiZeroBinsExact = 1 << kPhiJExact, kPhiZeroBinsLut = 1 << kPhiJLut;
 // Device copy: each bin (plus one all-zero sentinel bin) replicated kPhiCopies times,
 // interleaved, so the 8 threads of a quarter-warp LDS phase read 8 distinct bank groups.
 constexpr int kPhiCopies = 8;
@@ -88,7 +92,7 @@ struct metldpc_code_s {
     int32_t* d_cn_new = nullptr;
     int32_t* d_csr_ptr = nullptr;   // original CSR (int32) for the syndrome kernel (Step 1)
     int32_t* d_csr_vn = nullptr;
-    float* d_phi_exact = nullptr;   // (kPhiBinsExact + 1) * 8 copies * 4
-    float* d_phi_lut = nullptr;     // (kPhiBinsLut + 1) * 8 copies * 2
+    float* d_phi_exact = nullptr;   // (kPhiBinsExact + kPhiZeroBinsExact) * 8 copies * 4
+    float* d_phi_lut = nullptr;     // (kPhiBinsLut + kPhiZeroBinsLut) * 8 copies * 2
     int num_sms = 148;
 };

@@ -24,29 +24,29 @@ namespace metldpc {
 
 // ------------------------------------------------------------------ phi (N2)
 
-// Device table layout: [bin 0..NB (zero sentinel)][copy 0..7][coefficients]; a thread
+// Device table layout: [bin 0..NB-1, NB..NB+ZB-1 zero bins][copy 0..7][coefficients]; a thread
 // reads copy (lane & 7), so the 8 threads of an LDS phase hit 8 distinct bank groups
 // whatever their bins (no shared-memory bank conflicts, 1 wavefront per phase).
 template <int RULE>
 struct PhiT;
 template <>
 struct PhiT<METLDPC_RULE_EXACT> {      // cubic Hermite, 16 bins per binade
-    static constexpr int J = kPhiJExact, ENTRY = 16, NB = kPhiBinsExact;
+    static constexpr int J = kPhiJExact, ENTRY = 16, NB = kPhiBinsExact, ZB = kPhiZeroBinsExact;
     static constexpr int STRIDE = kPhiCopies * ENTRY;                        // bytes per bin
     static constexpr int BIAS = int(kPhiLoBits >> (23 - J)) * STRIDE;       // bin(2^-44) * STRIDE
-    static constexpr int TAB_BYTES = (NB + 1) * STRIDE;
+    static constexpr int TAB_BYTES = (NB + ZB) * STRIDE;
 };
 template <>
 struct PhiT<METLDPC_RULE_PHI_LUT> {    // linear, 32 bins per binade
-    static constexpr int J = kPhiJLut, ENTRY = 8, NB = kPhiBinsLut;
+    static constexpr int J = kPhiJLut, ENTRY = 8, NB = kPhiBinsLut, ZB = kPhiZeroBinsLut;
     static constexpr int STRIDE = kPhiCopies * ENTRY;
     static constexpr int BIAS = int(kPhiLoBits >> (23 - J)) * STRIDE;
-    static constexpr int TAB_BYTES = (NB + 1) * STRIDE;
+    static constexpr int TAB_BYTES = (NB + ZB) * STRIDE;
 };
 
 // phi(y), y >= 0, exactly as DESIGN.md N2: clamping the bit pattern to [2^-44, 2^6]
 // reproduces both out-of-range rules with no selects (u = 2^-44: bin 0, t = 0, c0 =
-// (float)phi(2^-44) = PHI_TOP; u = 2^6: the zero sentinel bin, +0).  The bin's byte
+// (float)phi(2^-44) = PHI_TOP; u = 2^6: the first zero bin, +0).  The bin's byte
 // offset is (u >> (23 - J)) * STRIDE = (u with the low 23-J bits cleared) >> 12.
 // The device table stores the coefficients pre-scaled by powers of two, c_k * 2^(J k),
 // and the polynomial runs in ts = t / 2^J = bits(1.0 | low mantissa bits) - 1 (exact):
@@ -199,14 +199,14 @@ __device__ __forceinline__ uint32_t cn_lane(uint32_t tabk, const float (&Lv)[NA 
     constexpr int D = NA + ND;
     const uint32_t one = one_bits();
     float p[D], P[D];
-    uint32_t xb[D];     // bits of x + 0.0f: sign bit = [x < 0] exactly (-0 + 0 = +0), N1 / R2
+    uint32_t xb[D];     // bits of x: sign bit = [x < 0] exactly (x is never -0, k_scatter), N1 / R2
     uint32_t par = sbit << 31;                            // bit 31: s_j XOR all n_k
     uint32_t chk = sbit ^ d1prev;
 #pragma unroll
     for (int s = 0; s < NA; ++s) {
         const float x = __fsub_rn(Lv[s], ro[s]);         // extrinsic q = L - r (R10)
-        chk ^= __float_as_uint(__fadd_rn(Lv[s], 0.0f)) >> 31;   // c_v^{l-1} = [L < 0] (-0 + 0 = +0)
-        xb[s] = __float_as_uint(__fadd_rn(x, 0.0f));
+        chk ^= __float_as_uint(Lv[s]) >> 31;             // c_v^{l-1} = [L < 0]: L is never -0 (k_scatter)
+        xb[s] = __float_as_uint(x);
         par ^= xb[s];
         p[s] = phi_dev<RULE>(tabk, fabsf(x), one);
     }
@@ -275,13 +275,14 @@ __device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
     return f2unpack(r);
 }
 
-// phi of two lanes: integer bin/mantissa work per lane, ts - 1 as one FADD2.
-template <int RULE>
+// phi of two lanes: integer bin/mantissa work per lane, ts - 1 as one FADD2.  UPPER = false:
+// the caller guarantees y < 2^7 (the zero bins above 2^6 then give phi = 0 with no clamp).
+template <int RULE, bool UPPER = true>
 __device__ __forceinline__ float2 phi_pair(uint32_t tabk, float y0, float y1, uint32_t one) {
     using P = PhiT<RULE>;
     constexpr uint32_t LOW = (1u << (23 - P::J)) - 1u;
-    const uint32_t u0 = phi_clamp_bits(y0);
-    const uint32_t u1 = phi_clamp_bits(y1);
+    const uint32_t u0 = UPPER ? phi_clamp_bits(y0) : __float_as_uint(fmaxf(y0, __uint_as_float(kPhiLoBits)));
+    const uint32_t u1 = UPPER ? phi_clamp_bits(y1) : __float_as_uint(fmaxf(y1, __uint_as_float(kPhiLoBits)));
     uint32_t e0, e1;
     asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(e0) : "r"(u0 >> (23 - P::J)), "n"(P::STRIDE), "r"(tabk));
     asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(e1) : "r"(u1 >> (23 - P::J)), "n"(P::STRIDE), "r"(tabk));
@@ -321,12 +322,11 @@ __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 
 #pragma unroll
     for (int s = 0; s < NA; ++s) {
         const float2 x = f2sub(Lv[s], ro[s]);                             // extrinsic q = L - r (R10)
-        const float2 Lz = f2add(Lv[s], zero2);                            // [L < 0] via sign of L + 0
-        chk0 ^= __float_as_uint(Lz.x) >> 31;
-        chk1 ^= __float_as_uint(Lz.y) >> 31;
-        const float2 xz = f2add(x, zero2);
-        xb0[s] = __float_as_uint(xz.x);
-        xb1[s] = __float_as_uint(xz.y);
+        // [L < 0] and [x < 0] are the sign bits: L and x are never -0 (see k_scatter)
+        chk0 ^= __float_as_uint(Lv[s].x) >> 31;
+        chk1 ^= __float_as_uint(Lv[s].y) >> 31;
+        xb0[s] = __float_as_uint(x.x);
+        xb1[s] = __float_as_uint(x.y);
         par0 ^= xb0[s];
         par1 ^= xb1[s];
         p[s] = phi_pair<RULE>(tabk, fabsf(x.x), fabsf(x.y), one);
@@ -352,7 +352,8 @@ __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 
             if (s > 0) Q = f2add(Q, p[s]);
             continue;
         }
-        const float2 ph = phi_pair<RULE>(tabk, S.x, S.y, one);
+        // S <= (D - 1) phi(2^-44) = 31.2 (D - 1) < 2^7 for D <= 5: no upper clamp needed
+        const float2 ph = phi_pair<RULE, (D > 5)>(tabk, S.x, S.y, one);
         const float2 o = make_float2(
             __uint_as_float(__float_as_uint(fminf(ph.x, kRMax)) | ((par0 ^ xb0[s]) & 0x80000000u)),
             __uint_as_float(__float_as_uint(fminf(ph.y, kRMax)) | ((par1 ^ xb1[s]) & 0x80000000u)));
@@ -554,19 +555,25 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
 // into registers or L1 all measured slower -- DESIGN.md section 7).  The tile's VN row offsets
 // are staged one tile ahead (double buffer).  One CTA per SM shares a single phi table; its
 // warp count is what the rings leave room for.
-constexpr int kPipeStages = 2;
+#ifndef METLDPC_PIPE_STAGES
+#define METLDPC_PIPE_STAGES 2   // shared-memory ring depth (3 stages measured no better)
+#endif
+#ifndef METLDPC_PIPE_WARPS
+#define METLDPC_PIPE_WARPS 32   // warps per CTA cap (at most what the rings leave room for)
+#endif
+constexpr int kPipeStages = METLDPC_PIPE_STAGES;
 constexpr int kSmemPerSm = 232448;     // opt-in dynamic shared memory per block (227 KB)
 
 template <int NA, int ND>
 struct PipeCfg {
     static constexpr int STG = (NA + ND) * 256;                       // bytes per stage: r, lambda
     static constexpr int IDX = 32 * NA;                               // ints per staged tile
-    static constexpr int WARP_BYTES = 2 * IDX * 4 + kPipeStages * STG + kPipeStages * 8;
+    static constexpr int WARP_BYTES = (2 * IDX * 4 + kPipeStages * STG + kPipeStages * 8 + 127) / 128 * 128;
     static constexpr int TAB = (PhiT<METLDPC_RULE_EXACT>::TAB_BYTES > PhiT<METLDPC_RULE_PHI_LUT>::TAB_BYTES)
                                    ? PhiT<METLDPC_RULE_EXACT>::TAB_BYTES
                                    : PhiT<METLDPC_RULE_PHI_LUT>::TAB_BYTES;
     static constexpr int W0 = (kSmemPerSm - TAB - 64) / WARP_BYTES;
-    static constexpr int WARPS = W0 > 32 ? 32 : W0;
+    static constexpr int WARPS = W0 > METLDPC_PIPE_WARPS ? METLDPC_PIPE_WARPS : W0;
     static constexpr int THREADS = WARPS * 32;
 };
 
@@ -1029,8 +1036,12 @@ __global__ void __launch_bounds__(256) k_scatter(CodeDev cd, Group g, const floa
         if (bad && lane == 0) atomicOr(g.invalid + c, bad);
         const int v = __ldg(cd.vmap + i);
         if (v >= 0) {
-            g.lam_a[size_t(v) * g.B + off] = val;
-            g.L[size_t(v) * 2 * g.B + off] = val;                    // L^0 = lambda (Step 2)
+            // lambda + 0: an input -0 becomes +0 (same value; R2 gives it no sign).  Then no L^l
+            // and no extrinsic L - r is ever -0 (L^l = lambda + sum, x = L - r with L != -0), so
+            // the CN kernels read [L < 0] and [x < 0] straight from the sign bits.
+            const float lz = __fadd_rn(val, 0.0f);
+            g.lam_a[size_t(v) * g.B + off] = lz;
+            g.L[size_t(v) * 2 * g.B + off] = lz;                     // L^0 = lambda (Step 2)
             g.L[size_t(v) * 2 * g.B + g.B + off] = 0.0f;             // empty VN-sum accumulator
         } else {
             g.lam1[size_t(~v) * g.B + off] = lam1_phi_form(cd, val);
@@ -1307,8 +1318,9 @@ __global__ void __launch_bounds__(256) k_refill_scatter(CodeDev cd, Group g, Str
         if (!mine) continue;
         const int v = __ldg(cd.vmap + i);
         if (v >= 0) {
-            g.lam_a[size_t(v) * g.B + off] = val;
-            g.L[size_t(v) * 2 * g.B + off] = val;
+            const float lz = __fadd_rn(val, 0.0f);      // -0 -> +0, as k_scatter
+            g.lam_a[size_t(v) * g.B + off] = lz;
+            g.L[size_t(v) * 2 * g.B + off] = lz;
             g.L[size_t(v) * 2 * g.B + g.B + off] = 0.0f;
         } else {
             g.lam1[size_t(~v) * g.B + off] = lam1_phi_form(cd, val);
