@@ -683,6 +683,7 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND>::THREADS, 1)
             if (k.check && on)
                 wv_l = __ldg(reinterpret_cast<const uint2*>(g.d1bits) + (size_t(k.rpar) * cd.n_1 + dbase + jt + lane));
         __syncwarp();
+        uint2 d1w = make_uint2(0u, 0u);   // degree-1 decision words of CN `lane` of the tile
         for (int i = 0; i < nt; ++i) {
             produce();
             const uint32_t st = nc % kPipeStages, ph = (nc / kPipeStages) & 1u;
@@ -726,13 +727,20 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND>::THREADS, 1)
             un1 |= __ballot_sync(FULL, c2.y);
             if constexpr (ND > 0) {
                 const uint32_t b0 = __ballot_sync(FULL, d1.x), b1 = __ballot_sync(FULL, d1.y);
-                if (lane == 0) {
-                    uint32_t* wp = g.d1bits + (size_t(k.wpar) * cd.n_1 + dbase + jl) * 2;
-                    wp[0] = (am0 == FULL) ? b0 : ((b0 & am0) | (wp[0] & ~am0));
-                    wp[1] = (am1 == FULL) ? b1 : ((b1 & am1) | (wp[1] & ~am1));
-                }
+                if (lane == i) { d1w.x = b0; d1w.y = b1; }   // lane i keeps CN i's words
             }
             __syncwarp();   // every lane has read stage st before it is refilled
+        }
+        if constexpr (ND > 0) {   // the tile's degree-1 decision words: one coalesced 8-byte store per lane
+            if (on) {
+                uint2* wp = reinterpret_cast<uint2*>(g.d1bits) + (size_t(k.wpar) * cd.n_1 + dbase + jt + lane);
+                if ((am0 & am1) != FULL) {   // keep the words of lanes not iterating
+                    const uint2 o = *wp;
+                    d1w.x = (d1w.x & am0) | (o.x & ~am0);
+                    d1w.y = (d1w.y & am1) | (o.y & ~am1);
+                }
+                *wp = d1w;
+            }
         }
     }
     if (k.check && lane == 0) {
