@@ -682,7 +682,11 @@ metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, cons
         cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, code->device);
         cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, code->device);
         const size_t rows = 2 * size_t(L.n_a) * B * sizeof(float);
-        if (!(e && *e == '0') && d->K == 1 && max_persist > 0 && max_window > 0) {
+        // Only when the rows fit the set-aside: a window larger than it (no-skip layouts, whose
+        // rows are ~8x larger) keeps a fraction of the rows persisting and starves the streams
+        // (measured: no-skip C3 CN phase 0.68 -> 1.51 ms).
+        if (!(e && *e == '0') && d->K == 1 && max_persist > 0 && max_window > 0 && rows <= size_t(max_persist) &&
+            rows <= size_t(max_window)) {
             const size_t want = std::min(size_t(max_persist), rows * size_t(d->K));
             cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
             for (int k = 0; k < d->K; ++k) {
