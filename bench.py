@@ -329,16 +329,24 @@ def main():
     peak, peak_src = measured_peak_gbs()
     cn_gbs = prof_k["cn_lane_iters"] * bm["cn"] / (prof_k["cn_ms"] / 1e3) / 1e9 if prof_k["cn_ms"] > 0 else None
     vn_gbs = prof_k["cn_lane_iters"] * bm["vn"] / (prof_k["vn_ms"] / 1e3) / 1e9 if prof_k["vn_ms"] > 0 else None
-    traffic = None
+    # ncu DRAM bytes of the CN phase, captured for one workload (profiles/cn_traffic.json):
+    # reported only on a line of that workload
+    traffic = traffic_prod = None
     tpath = ROOT / "profiles" / "cn_traffic.json"
     if tpath.exists():
         try:
-            traffic = json.loads(tpath.read_text()).get("dram_bytes_per_launch")
+            tj = json.loads(tpath.read_text())
+            w = tj.get("workload", {})
+            if (w.get("family"), w.get("n"), w.get("no_skip", False), w.get("lanes", 64)) == \
+                    (a.family, a.n, bool(a.no_skip), a.lanes):
+                traffic = tj.get("dram_bytes_per_launch")
+                traffic_prod = tj.get("production_graph", {}).get("dram_bytes_per_pass")
         except Exception:
-            traffic = None
+            traffic = traffic_prod = None
     it_bytes = F * world * a.steps * a.iters
     roofline = {"bound": "hbm", "achieved": cn_gbs, "peak": peak, "unit": "GB/s",
                 "frac": (cn_gbs / peak) if cn_gbs else None, "traffic": traffic,
+                "traffic_production_pass": traffic_prod,
                 "kernel": "CN phase: k_cn_pipe + k_cn_tile launches of one iteration (all degree classes, VN sums fused)",
                 "bytes_per_launch": bm["cn"] * min(F, a.lanes), "peak_source": peak_src,
                 "avg_launch_ms": prof_k["cn_ms"] / max(1, prof_k["cn_launches"]), "kernel_timing": kernel_timing,
