@@ -195,7 +195,9 @@ metldpc_status metldpc_syndrome(metldpc_decoder dec, int32_t batch, const uint32
  *   llr        dev fp32 [batch][n]         lambda per frame, original VN order
  *   syndrome   dev u32  [batch][ceil(m/32)] Bob's S_B per frame (Step 1)
  *   max_iter   1..cfg.max_iter, or 0 => cfg.max_iter
- *   bits_out   dev u32  [batch][ceil(n/32)] hard decisions c, original VN order
+ *   bits_out   dev u32  [batch][ceil(n/32)] hard decisions c, original VN order (Step 5,
+ *                                c = [posterior LLR < 0]; a degree-1 VN's posterior
+ *                                is lambda + its unclamped CN output, N1 / R27)
  *   iters_out  dev i32  [batch]  first l in 1..max_iter with H c^l = S_B (early_term),
  *                                else max_iter; -1 if the frame's lambda has a non-finite
  *                                value (R24; bits are then 0)
