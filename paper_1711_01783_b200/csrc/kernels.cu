@@ -573,7 +573,10 @@ struct PipeCfg {
                                    ? PhiT<METLDPC_RULE_EXACT>::TAB_BYTES
                                    : PhiT<METLDPC_RULE_PHI_LUT>::TAB_BYTES;
     static constexpr int W0 = (kSmemPerSm - TAB - 64) / WARP_BYTES;
-    static constexpr int WARPS = W0 > METLDPC_PIPE_WARPS ? METLDPC_PIPE_WARPS : W0;
+    // NA = 4 (the no-skip layouts' inner checks) spills at 64 registers (32 warps): 24 warps with
+    // 80 registers measured 810 vs 715 Mb/s on no-skip C3
+    static constexpr int WCAP = NA >= 4 ? 24 : METLDPC_PIPE_WARPS;
+    static constexpr int WARPS = W0 > WCAP ? WCAP : W0;
     static constexpr int THREADS = WARPS * 32;
 };
 
