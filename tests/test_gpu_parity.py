@@ -286,6 +286,42 @@ def test_generic_degree_paths_and_alist(tmp_path):
     assert windows == {0, 1, 2, 3, 4}, windows
 
 
+def _degree1_edge_code():
+    """CN 0, 1: VNs 0-2 (active) + one degree-1 VN each -> the (3,1) pipelined class;
+    CN 2: VN 0 + two degree-1 VNs -> the generic class; CN 3: VNs 1, 2 + VN 0."""
+    h = np.zeros((4, 8), np.uint8)
+    h[0, [0, 1, 2, 3]] = 1
+    h[1, [0, 1, 2, 4]] = 1
+    h[2, [0, 5, 6]] = 1
+    h[3, [0, 1, 2, 7]] = 1
+    return from_dense(h)
+
+
+@pytest.mark.parametrize("rule", RULES)
+def test_degree1_decision_edge_cases(rule):
+    """Degree-1 decisions (N1, R27) through the pipelined and the generic CN kernels, bit-exact
+    against M3 on crafted priors: signed zeros, exact ties, |lambda| around the 30 clamp and far
+    beyond the phi table, tiny values; 1-4 iterations, ET on and off."""
+    code = _degree1_edge_code()
+    hd = B.Code(code)
+    rng = np.random.default_rng(27)
+    special = np.array([0.0, -0.0, 30.5, -30.5, 31.0, -29.9, 32.0, 64.0, -70.0, 1e6, -1e6, 1e-30, -1e-30,
+                        0.5, -0.5, 3.0], np.float32)
+    n = code.n
+    llr = rng.choice(special, size=(64, n)).astype(np.float32)
+    llr[32:] = rng.normal(0.0, 4.0, (32, n)).astype(np.float32)
+    llr[40:44, :3] = 32.0                     # inputs whose CN output exceeds the clamp
+    llr[40:44, 3] = np.float32(-30.5)
+    llr[44:48, 3] = -llr[44:48, 0]            # ties between a prior and a message
+    synd = np.stack([pack_bits(rng.integers(0, 2, code.m)) for _ in range(64)])
+    for et in (True, False):
+        for it in (1, 2, 4):
+            _, bits, iters, conv = _gpu_decode(hd, llr, synd, rule, it, et=et)
+            for i in range(64):
+                o = bp.decode(code, llr[i], synd[i], it, early_term=et, rule=rule, prec=32)
+                _assert_frame_equal(code, o, bits[i], iters[i], conv[i], f"frame {i} N {it} et {et}")
+
+
 def test_empty_check_row():
     """A degree-0 CN with S_B bit 1 can never be satisfied (R23)."""
     h = np.array([[1, 1, 0, 0], [0, 1, 1, 1], [0, 0, 0, 0]], np.uint8)
