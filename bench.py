@@ -340,13 +340,20 @@ def main():
             if (w.get("family"), w.get("n"), w.get("no_skip", False), w.get("lanes", 64)) == \
                     (a.family, a.n, bool(a.no_skip), a.lanes):
                 traffic = tj.get("dram_bytes_per_launch")
-                traffic_prod = tj.get("production_graph", {}).get("dram_bytes_per_pass")
+                pg = tj.get("production_graph", {})
+                traffic_prod = pg.get("dram_bytes_per_pass")
+                if traffic_prod and pg.get("graph_ms_per_pass"):
+                    # SURVEY 8(d)'s second fraction: ncu-measured DRAM bytes / time of a whole
+                    # production pass (same capture), against the same peak
+                    traffic_prod = {"bytes": traffic_prod, "ms": pg["graph_ms_per_pass"],
+                                    "dram_gbs": traffic_prod / pg["graph_ms_per_pass"] / 1e6}
         except Exception:
             traffic = traffic_prod = None
     it_bytes = F * world * a.steps * a.iters
     roofline = {"bound": "hbm", "achieved": cn_gbs, "peak": peak, "unit": "GB/s",
                 "frac": (cn_gbs / peak) if cn_gbs else None, "traffic": traffic,
-                "traffic_production_pass": traffic_prod,
+                "traffic_production_pass": (dict(traffic_prod, frac=traffic_prod["dram_gbs"] / peak)
+                                            if isinstance(traffic_prod, dict) and peak else traffic_prod),
                 "kernel": "CN phase: k_cn_pipe + k_cn_tile launches of one iteration (all degree classes, VN sums fused)",
                 "bytes_per_launch": bm["cn"] * min(F, a.lanes), "peak_source": peak_src,
                 "avg_launch_ms": prof_k["cn_ms"] / max(1, prof_k["cn_launches"]), "kernel_timing": kernel_timing,
