@@ -220,11 +220,95 @@ def run_reference(a, rank: int, world: int):
     print(json.dumps(out), flush=True)
 
 
+# ----------------------------------------------------------------------------- rank logic (shared with tests)
+
+def spawn_ranks(a) -> int | None:
+    """`python bench.py --gpus N` without a torchrun environment: launch N ranks (one per GPU)
+    through torch.distributed.run on 127.0.0.1 and return its exit code; None if this process
+    is already a rank (or N = 1)."""
+    if a.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def rank_frame_ids(n_distinct: int, rank: int, world: int):
+    """Global frame ids of this rank: f with f mod world == rank."""
+    from paper_1711_01783_b200 import dist as D
+    return D.shard_frames(range(n_distinct * world), rank, world)
+
+
+def timed_steps(step, steps: int, warmup: int, sync, barrier, timer, on_start=None) -> float:
+    """W untimed warm-up steps, then EXACTLY K timed steps bracketed by barrier + sync on
+    both sides; step(i) gets the timed step's index (None during warm-up); on_start runs
+    between the warm-up and the timed region.  Returns this rank's time in ms from `timer`
+    (CUDA events on the launch stream in bench)."""
+    for _ in range(max(warmup, 0)):
+        step(None)
+    sync()
+    if on_start is not None:
+        on_start()
+        sync()
+    barrier()
+    t = timer
+    t.start()
+    for i in range(steps):
+        step(i)
+    t.stop()
+    sync()
+    barrier()
+    return t.ms()
+
+
+def gather_frames(iters, conv, world: int):
+    """All-gather of the per-frame (iterations, converged) of the last step:
+    returns int64 [world * F] arrays in global frame order (rank r's local frame i is
+    global frame i * world + r, the f mod world sharding)."""
+    import torch
+    import torch.distributed as dist
+    pair = torch.stack([iters.to(torch.int32), conv.to(torch.int32)]).contiguous()   # [2, F]
+    if world > 1:
+        parts = [torch.empty_like(pair) for _ in range(world)]
+        dist.all_gather(parts, pair)
+        out = torch.stack(parts)
+    else:
+        out = pair[None]
+    out = out.cpu().numpy()                                                     # [world, 2, F]
+    glob = out.transpose(1, 2, 0).reshape(2, -1)                                # frame i*world + r
+    return glob[0].astype(np.int64), glob[1].astype(np.int64)
+
+
+def summarize_counts(total, it_glob, cv_glob, frames_per_step: int) -> dict:
+    """Counters summed over ranks and timed steps (k_counters + all-reduce), plus the
+    per-frame picture of the last step from the all-gather."""
+    frames_c, conv_c, iters_c, bad_c = (int(x) for x in total)
+    valid = it_glob >= 0
+    hist = np.bincount(it_glob[valid], minlength=1)
+    return {"frames_timed": frames_c, "converged_timed": conv_c, "invalid_timed": bad_c,
+            "fer": 1.0 - conv_c / max(1, frames_c), "mean_iters": iters_c / max(1, frames_c - bad_c),
+            "last_step_frames": int(it_glob.size), "last_step_converged": int(cv_glob.sum()),
+            "last_step_iters_hist": {str(k): int(v) for k, v in enumerate(hist) if v},
+            "frames_per_step": frames_per_step}
+
+
+# ----------------------------------------------------------------------------- main
+
 def main():
     a = parse()
+    rc = spawn_ranks(a) if a.impl == "ours" else None   # the reference arm is rank 0 alone
+    if rc is not None:
+        sys.exit(rc)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if world != a.gpus and "WORLD_SIZE" in os.environ:
+        raise SystemExit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}")
     if a.impl == "reference":
         return run_reference(a, rank, world)
 
@@ -240,17 +324,21 @@ def main():
         build()
     torch.cuda.set_device(local)
     if world > 1:
+        # the communicator's init lines (nranks, NVLS) go to stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist.barrier()
         if rank != 0:
             build()
+        assert dist.get_world_size() == a.gpus
     dev = torch.device("cuda", local)
     code = make_met_code(a.family, a.n)
     st = code.stats()
     F = a.frames
     # frames of this rank: global ids f with f mod world == rank; ND distinct ones tiled to F
     ND = min(a.distinct, F)
-    ids = D.shard_frames(range(ND * world), rank, world)
+    ids = rank_frame_ids(ND, rank, world)
     v_np, xn_np, sy_np = gen_frames(a, ids)
     rep = (F + ND - 1) // ND
     v = torch.from_numpy(np.tile(v_np, (rep, 1))[:F]).to(dev)
@@ -266,44 +354,49 @@ def main():
     bits = torch.empty((F, nw), dtype=torch.int32, device=dev)
     iters = torch.empty(F, dtype=torch.int32, device=dev)
     conv = torch.empty(F, dtype=torch.uint8, device=dev)
-    cnt = torch.zeros(4, dtype=torch.int64, device=dev)
+    # one counter row per timed step (metldpc_batch_counters adds into its row; the row is
+    # then all-reduced over the ranks -- the step's only exchange); warm-up uses a scratch row
+    cnt = torch.zeros((a.steps + 1, 4), dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream()
 
-    def step():
+    def step(i):
+        row = cnt[a.steps if i is None else i]
         dec.llr_from_md(v, xn, a.snr, out=llr)
         dec.decode(llr, sy, out=(bits, iters, conv))
-        dec.counters(iters, conv, cnt)
-        D.reduce_counters(cnt)          # NCCL all-reduce when world > 1 (the only exchange)
+        dec.counters(iters, conv, row)
+        D.reduce_counters(row)          # NCCL all-reduce when world > 1
 
-    for _ in range(max(a.warmup, 0)):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    cnt.zero_()
-    dec.reset_profile()
+    class CudaTimer:
+        def start(self):
+            self.e0 = torch.cuda.Event(enable_timing=True)
+            self.e1 = torch.cuda.Event(enable_timing=True)
+            self.e0.record(stream)
+
+        def stop(self):
+            self.e1.record(stream)
+
+        def ms(self):
+            return self.e0.elapsed_time(self.e1)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
     dec.set_profiling(False)              # the timed region runs the production path (graph loop)
-    launches0 = dec.profile()["launches"]
-    sampler = ClockSampler(local) if local == 0 or world == 1 else None
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    e0.record(stream)
-    for _ in range(a.steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    holder = {}
+
+    def on_start():                       # after warm-up: zero the launch count, start the clock sampler
+        dec.reset_profile()
+        holder["s"] = ClockSampler(local) if local == 0 or world == 1 else None
+
+    ms_rank = timed_steps(step, a.steps, a.warmup, torch.cuda.synchronize, barrier, CudaTimer(), on_start)
+    sampler = holder.get("s")
     clocks = sampler.stop() if sampler else None
-    dec.set_profiling(False)
     prof = dec.profile()
-    ms_max = D.max_over_ranks(e0.elapsed_time(e1), device=dev)
-    counters = cnt.cpu().numpy()   # all-reduced in-step when world > 1 (sum over ranks of K steps)
-    if world == 1:
-        pass
+    ms_max = D.max_over_ranks(ms_rank, device=dev)
+    total = cnt[:a.steps].sum(0).cpu().numpy()           # already summed over ranks per step
+    it_glob, cv_glob = gather_frames(iters, conv, world)
+    counts = summarize_counts(total, it_glob, cv_glob, F * world)
     frames_total = F * world * a.steps
     value = frames_total * a.n / (ms_max / 1e3) / 1e6
 
@@ -328,7 +421,6 @@ def main():
     bm = metrics.bytes_per_cw_iter(st["iter_edges"], st["n_deg1"], st["n_active"], st["m"])
     peak, peak_src = measured_peak_gbs()
     cn_gbs = prof_k["cn_lane_iters"] * bm["cn"] / (prof_k["cn_ms"] / 1e3) / 1e9 if prof_k["cn_ms"] > 0 else None
-    vn_gbs = prof_k["cn_lane_iters"] * bm["vn"] / (prof_k["vn_ms"] / 1e3) / 1e9 if prof_k["vn_ms"] > 0 else None
     # ncu DRAM bytes of the CN phase, captured for one workload (profiles/cn_traffic.json):
     # reported only on a line of that workload
     traffic = traffic_prod = None
@@ -337,8 +429,8 @@ def main():
         try:
             tj = json.loads(tpath.read_text())
             w = tj.get("workload", {})
-            if (w.get("family"), w.get("n"), w.get("no_skip", False), w.get("lanes", 64)) == \
-                    (a.family, a.n, bool(a.no_skip), a.lanes):
+            if (w.get("family"), w.get("n"), w.get("no_skip", False), w.get("lanes", 64), w.get("rule", "exact")) == \
+                    (a.family, a.n, bool(a.no_skip), a.lanes, a.rule):
                 traffic = tj.get("dram_bytes_per_launch")
                 pg = tj.get("production_graph", {})
                 traffic_prod = pg.get("dram_bytes_per_pass")
@@ -355,12 +447,15 @@ def main():
                 "traffic_production_pass": (dict(traffic_prod, frac=traffic_prod["dram_gbs"] / peak)
                                             if isinstance(traffic_prod, dict) and peak else traffic_prod),
                 "kernel": "CN phase: k_cn_pipe + k_cn_tile launches of one iteration (all degree classes, VN sums fused)",
-                "bytes_per_launch": bm["cn"] * min(F, a.lanes), "peak_source": peak_src,
+                "bytes_per_launch": bm["cn"] * min(F, a.lanes),
+                "bytes_model": "s(2 E_it + n_1 + n_a) + m/8 per codeword-iteration (SURVEY 8(d) without the "
+                               "VN write-back, which the fused VN sum keeps in L2), x 64 lanes",
+                "peak_source": peak_src,
                 "avg_launch_ms": prof_k["cn_ms"] / max(1, prof_k["cn_launches"]), "kernel_timing": kernel_timing,
-                "vn_update": {"achieved": vn_gbs, "frac": (vn_gbs / peak) if vn_gbs else None,
-                              "avg_launch_ms": prof_k["vn_ms"] / max(1, prof_k["vn_launches"])},
-                "iteration_alg_frac": (it_bytes * bm["alg"] / (ms_max / 1e3) / 1e9 / peak),
-                "iteration_two_pass_frac": (it_bytes * bm["two_pass"] / (ms_max / 1e3) / 1e9 / peak)}
+                "finish_avg_launch_ms": prof_k["vn_ms"] / max(1, prof_k["vn_launches"]),
+                # whole timed step: the method's algorithmic floor (SURVEY 8(d) B_alg) x codeword-
+                # iterations (N per frame: every frame runs N at this SNR when none converges)
+                "iteration_alg_frac": (it_bytes * bm["alg"] / (ms_max / 1e3) / 1e9 / peak)}
 
     # ---- e2e through the host-buffer C-ABI call (pinned host memory, copies inside)
     e2e = None
@@ -371,8 +466,7 @@ def main():
         out_h = (torch.empty((F, nw), dtype=torch.int32).pin_memory(), torch.empty(F, dtype=torch.int32).pin_memory(),
                  torch.empty(F, dtype=torch.uint8).pin_memory())
         dec.decode_md_host(v_h, xn_h, sy_h, a.snr, out=out_h)      # warm (allocates staging)
-        if world > 1:
-            dist.barrier()
+        barrier()
         k_e2e = max(1, min(a.steps, 3))
         t0 = time.perf_counter()
         for _ in range(k_e2e):
@@ -382,20 +476,25 @@ def main():
         e2e = {"value": F * world * k_e2e * a.n / dt / 1e6, "unit": "Mb/s",
                "h2d_bytes_per_step": F * world * (a.n * 4 + (a.n // 8) * 4 + W * 4),
                "d2h_bytes_per_step": F * world * (nw * 4 + 4 + 1),
-               "api": "metldpc_decode_md_host (pinned host buffers; H2D, LLR, decode, D2H per 64-lane group, "
-                      "copies overlapped with decode)", "steps": k_e2e}
+               "api": "metldpc_decode_md_host (pinned host buffers; H2D, LLR, decode, D2H inside the call; "
+                      + ("lane refill: chunked H2D published to the streaming decode's queue"
+                         if not (a.no_refill or a.no_et) else "64-lane groups, copies overlapped with decode") + ")",
+               "steps": k_e2e, "timing": "host wall clock around the synchronous call, max over ranks"}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         cpu = oracle_throughput(a, code, v_np, xn_np, sy_np, a.cpu_budget)
 
     if rank == 0:
-        frames_c, conv_c, iters_c, bad_c = (int(x) for x in counters)
         R = (a.n - st["m"]) / a.n
+        conv_frac = counts["converged_timed"] / max(1, counts["frames_timed"])
         out = {
             "metric": METRIC, "value": value, "unit": "Mb/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": (value / paper_mbps(a)) if paper_mbps(a) else None, "dtype": "f32", "data": "synthetic",
+            "value_definition": "n-bit Mb/s: all n decoded bits of every frame per second, converged or not -- "
+                                "the paper's Table-1 'Error Correction Speed' n/(N x latency) (P:69-72); "
+                                "info_mbps = R x value, goodput_info_mbps = R x n x converged frames / s",
             "config": {"workload": workload_name(a), "code": f"{a.family} stand-in (Table-1 counts), n={a.n}, "
                        f"m={st['m']}, E={st['edges']}, E_it={st['iter_edges']}", "snr": a.snr,
                        "beta": metrics.beta(R, a.snr), "max_iter": a.iters, "early_term": not a.no_et,
@@ -403,15 +502,17 @@ def main():
                        "lanes_per_group": a.lanes, "groups_in_flight": a.groups, "global_batch": F * world,
                        "lane_refill": not a.no_refill,
                        "l2": "inputs larger than L2 (v 1 GB, edge messages 740 MB per 64-lane group)",
-                       "parallelism": f"dp{world} (frames sharded f mod G; NCCL all-reduce of FER counters)"},
+                       "parallelism": f"dp{world} (frames sharded f mod G; per-step NCCL all-reduce of the FER "
+                                      "counters, one all-gather of per-frame results)"},
             "baseline_context": (f"vs_baseline = value / {paper_mbps(a)} Mb/s: paper Table 1 rate "
                                  f"{a.family[1:]} {'without' if a.no_skip else 'with'} skipping on one TITAN Xp "
                                  "(64 codewords, fixed N iterations) -- context, other hardware")
                                 if paper_mbps(a) else None,
-            "info_mbps": value * R, "fer": 1.0 - conv_c / max(1, frames_c), "mean_iters": iters_c / max(1, frames_c - bad_c),
-            "frames_timed": frames_c,
+            "info_mbps": value * R, "goodput_info_mbps": value * R * conv_frac,
+            **counts,
+            "comm": {"backend": "nccl" if world > 1 else None, "world_size": world},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(prof["launches"] - launches0), "clocks": clocks,
+            "gpu_launches": int(prof["launches"]), "clocks": clocks,
         }
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -140,6 +140,9 @@ metldpc_status metldpc_code_check(int32_t n, int32_t m, int64_t num_edges,
 
 metldpc_status metldpc_code_info(metldpc_code code, metldpc_code_info_t* out);
 
+/* (EUNSUPPORTED also if a VN has degree > 512: the exact fixed-point VN sum of DESIGN.md N3
+ * would overflow its 32-bit accumulator.) */
+
 /* Destroy after every decoder using it. NULL is a no-op. */
 void metldpc_code_destroy(metldpc_code code);
 
@@ -246,6 +249,14 @@ metldpc_status metldpc_batch_counters(metldpc_decoder dec, int32_t batch, const 
  * (CSR order with degree-1 edges removed), L_out [n_active] in ascending VN index order.
  * With early_term = 0 and max_iter = l this is (r^l, L^l).  Synchronises the device. */
 metldpc_status metldpc_debug_dump(metldpc_decoder dec, int32_t lane, float* r_out, float* L_out);
+
+/* Run k (>= 1) further iterations on the state left by the last decode (P:117-146 Steps 3-4;
+ * SURVEY 8(b) debug hook): the valid lanes of the last lane group are re-activated and k plain
+ * iterations (CN update, VN update; no syndrome test, no latch) are enqueued on cuda_stream.
+ * With early_term = 0 and max_iter = l - 1, metldpc_debug_dump before and after one step
+ * gives (r^{l-1}, L^{l-1}) and (r^l, L^l) -- the teacher-forced comparison with the fp64
+ * definition.  EINVAL before any decode or after a streaming (lane-refill) decode. */
+metldpc_status metldpc_debug_step(metldpc_decoder dec, int32_t k, uintptr_t cuda_stream);
 
 /* The fp32 phi table of a rule (N2), host computed, no GPU touched:
  * EXACT 800 x 4 floats (c0..c3 per bin, 16 bins per binade), PHI_LUT 1600 x 2 floats

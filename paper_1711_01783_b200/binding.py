@@ -81,6 +81,7 @@ SYMBOLS = {
                                          C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "metldpc_batch_counters": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]),
     "metldpc_debug_dump": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    "metldpc_debug_step": (C.c_int, [C.c_void_p, C.c_int32, C.c_size_t]),
     "metldpc_phi_table": (C.c_int32, [C.c_int32, C.c_void_p, C.c_int32]),
     "metldpc_set_profiling": (C.c_int, [C.c_void_p, C.c_int32]),
     "metldpc_get_profile": (C.c_int, [C.c_void_p, C.POINTER(Profile)]),
@@ -221,6 +222,10 @@ def metldpc_debug_dump(dec, lane, r_out, L_out):
     _check(lib().metldpc_debug_dump(dec, lane, _ptr(r_out), _ptr(L_out)), "metldpc_debug_dump")
 
 
+def metldpc_debug_step(dec, k, stream=None):
+    _check(lib().metldpc_debug_step(dec, k, _stream(stream)), "metldpc_debug_step")
+
+
 def metldpc_phi_table(rule):
     import numpy as np
     need = lib().metldpc_phi_table(rule, None, 0)
@@ -359,6 +364,9 @@ class Decoder:
         L = np.zeros(self.code.info.n_active, np.float32)
         metldpc_debug_dump(self.h, lane, r, L)
         return r, L
+
+    def step(self, k: int = 1, stream=None):
+        metldpc_debug_step(self.h, k, stream)
 
     def set_profiling(self, on: bool):
         metldpc_set_profiling(self.h, on)

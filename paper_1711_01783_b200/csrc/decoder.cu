@@ -67,6 +67,8 @@ struct metldpc_decoder_s {
     std::vector<cudaStream_t> gs;                   // one stream per workspace (K > 1)
     std::vector<cudaEvent_t> fork_ev, join_ev;
     int last_ws = 0;                                // workspace of the last group decoded
+    int last_nb = 0;                                // its frames (group mode)
+    bool last_streaming = false;                    // the last decode was a streaming decode
     // host-path staging: 2 rounds x K groups
     struct Staging {
         float* llr = nullptr;
@@ -77,6 +79,16 @@ struct metldpc_decoder_s {
         float* xnorm = nullptr;
     };
     std::vector<Staging> st;
+    size_t st_xnorm_cap = 0;                        // floats per group-mode slot's xnorm buffer
+    struct HostStream {                             // streaming host path: up to kHostStreamCap frames
+        float* llr = nullptr;
+        uint32_t* synd = nullptr;
+        uint32_t* bits = nullptr;
+        int32_t* iters = nullptr;
+        uint8_t* conv = nullptr;
+        float* xnorm = nullptr;
+        size_t xnorm_cap = 0;
+    } hs;
     cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
     // accounting
     int profiling = 0;
@@ -302,6 +314,8 @@ metldpc_status group_end(metldpc_decoder d, const GroupJob& j, int N) {
     launch_finalize(cd, g, j.nb, j.bits_out, j.iters_out, j.conv_out, j.s);
     d->prof.launches += 3;
     d->last_ws = j.k;
+    d->last_nb = j.nb;
+    d->last_streaming = false;
     CUDA_TRY(cudaGetLastError());
     return METLDPC_OK;
 }
@@ -440,7 +454,7 @@ metldpc_status stream_graph(metldpc_decoder d, int k, cudaGraphExec_t* out) {
     // part C: pass counter and loop condition, after the IF node
     if ((e = cudaStreamBeginCaptureToGraph(cs, body, &inode, nullptr, 1, cudaStreamCaptureModeRelaxed)) != cudaSuccess)
         return fail_capture(e, "stream graph capture: ");
-    launch_stream_ctl(g, (unsigned long long)hw, cs);
+    launch_stream_ctl(g, d->job, (unsigned long long)hw, cs);
     if ((e = cudaStreamEndCapture(cs, &cap)) != cudaSuccess) return fail_capture(e, "stream graph capture: ");
     cudaStreamDestroy(cs);
     cudaGraphExec_t exec;
@@ -457,11 +471,13 @@ bool stream_mode(metldpc_decoder d) {
 }
 
 // Streaming decode of a whole batch: every workspace runs its refill graph on its own stream,
-// all drawing frames from one device-side queue (StreamJob::next).
-metldpc_status stream_decode(metldpc_decoder d, int32_t batch, const float* llr, const uint32_t* synd, int N,
-                             uint32_t* bits_out, int32_t* iters_out, uint8_t* conv_out, cudaStream_t s) {
-    const CodeDev cd = code_dev(d->code, d->cfg.rule);
-    StreamJob h{};
+// all drawing frames from one device-side queue (StreamJob::next).  Two stream-ordered parts:
+// stream_setup writes the queue header (frames [0, avail) already on the device; the host path
+// passes 0 and raises it with k_publish as its copies land), stream_launch starts the graphs.
+metldpc_status stream_setup(metldpc_decoder d, int32_t batch, const float* llr, const uint32_t* synd, int N,
+                            uint32_t* bits_out, int32_t* iters_out, uint8_t* conv_out, int32_t avail,
+                            cudaStream_t s) {
+    StreamJob h{};   // pageable source: cudaMemcpyAsync stages it before returning
     h.llr = llr;
     h.synd = synd;
     h.bits = bits_out;
@@ -470,11 +486,20 @@ metldpc_status stream_decode(metldpc_decoder d, int32_t batch, const float* llr,
     h.nframes = batch;
     h.next = 0;
     h.N = N;
+    h.avail = avail;
     {
         const char* e = std::getenv("METLDPC_REFILL_MIN");
         h.wave_min = (e && std::atoi(e) > 0) ? std::atoi(e) : 16;
     }
+    // hang guard only: a lane needs at most N + 1 passes per frame
+    const int64_t guard = (int64_t(batch) + d->B) * (int64_t(N) + 2) + 1000;
+    h.max_passes = int32_t(std::min<int64_t>(guard, INT32_MAX));
     CUDA_TRY(cudaMemcpyAsync(d->job, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+    return METLDPC_OK;
+}
+
+metldpc_status stream_launch(metldpc_decoder d, int32_t batch, cudaStream_t s) {
+    const CodeDev cd = code_dev(d->code, d->cfg.rule);
     const int K = std::min(d->K, (batch + d->B - 1) / d->B);
     if (K > 1) {
         CUDA_TRY(cudaEventRecord(d->fork_ev[0], s));
@@ -492,6 +517,7 @@ metldpc_status stream_decode(metldpc_decoder d, int32_t batch, const float* llr,
         d->prof.launches += 1;                   // + passes and waves, counted on the device
         d->stream_used = true;
         d->last_ws = k;
+        d->last_streaming = true;
     }
     if (K > 1)
         for (int k = 0; k < K; ++k) {
@@ -778,6 +804,12 @@ void metldpc_decoder_destroy(metldpc_decoder d) {
         dfree(sl.conv);
         dfree(sl.xnorm);
     }
+    dfree(d->hs.llr);
+    dfree(d->hs.synd);
+    dfree(d->hs.bits);
+    dfree(d->hs.iters);
+    dfree(d->hs.conv);
+    dfree(d->hs.xnorm);
     if (d->s_h2d) cudaStreamDestroy(d->s_h2d);
     if (d->s_comp) cudaStreamDestroy(d->s_comp);
     if (d->s_d2h) cudaStreamDestroy(d->s_d2h);
@@ -860,7 +892,10 @@ metldpc_status metldpc_decode(metldpc_decoder d, int32_t batch, const float* llr
     const HostLayout& L = d->code->host;
     const size_t W = size_t(L.m + 31) / 32, NW = size_t(L.n + 31) / 32;
     const int groups = (batch + d->B - 1) / d->B;
-    if (stream_mode(d)) return stream_decode(d, batch, llr, syndrome, N, bits_out, iters_out, conv_out, s);
+    if (stream_mode(d)) {
+        metldpc_status st = stream_setup(d, batch, llr, syndrome, N, bits_out, iters_out, conv_out, batch, s);
+        return st ? st : stream_launch(d, batch, s);
+    }
     if (d->K > 1 && d->use_graph && !d->profiling && groups > d->K) {
         // Group queue: workspace k decodes groups k, k + K, ... on its own stream with no
         // per-round join, so with early termination a workspace whose group finished early
@@ -897,136 +932,250 @@ metldpc_status metldpc_decode(metldpc_decoder d, int32_t batch, const float* llr
 
 namespace {
 
-// Host-buffer pipeline shared by metldpc_decode_host (LLR input) and
-// metldpc_decode_md_host (MD output input).  Groups are decoded in rounds of K (the
-// concurrent workspaces); staging is double-buffered across rounds, so the H2D of round
-// r+1 and the D2H of round r-1 run on their own streams while round r decodes.
+// Host-buffer paths (metldpc_decode_host: LLR input; metldpc_decode_md_host: MD output input).
+//
+// Streaming (lane refill, the default with early termination): the batch is copied to device
+// staging in chunks on the copy stream -- each chunk's H2D, its LLR conversion, then k_publish
+// raising the queue's `avail` -- while the streaming decode (stream_launch) already runs on the
+// compute stream from the first chunk on; freed lanes take frames as they become available.
+// Results go to device staging (k_finalize_lanes) and come back in one D2H per super-chunk.
+// Batches larger than the staging capacity run as consecutive super-chunks.
+//
+// Group mode (lane_refill = 0, early_term = 0 or profiling): groups are decoded in rounds of K
+// workspaces with staging double-buffered across rounds, so the H2D of round r+1 and the D2H of
+// round r-1 run on their own streams while round r decodes.
+//
+// Every CUDA call's status is checked; the first failure stops the enqueueing, the streams are
+// drained and ECUDA is returned.
+#define HP(expr)                                                               \
+    do {                                                                       \
+        if (ce == cudaSuccess) {                                               \
+            ce = (expr);                                                       \
+            if (ce != cudaSuccess) what = #expr;                               \
+        }                                                                      \
+    } while (0)
+
+constexpr int kHostStreamCap = 2048;   // frames staged at once by the streaming host path
+constexpr int kHostChunk = 32;         // frames per H2D chunk (one k_publish each)
+
+metldpc_status ensure_host_streams(metldpc_decoder d) {
+    if (d->s_comp) return METLDPC_OK;
+    CUDA_TRY(cudaStreamCreateWithFlags(&d->s_h2d, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&d->s_comp, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&d->s_d2h, cudaStreamNonBlocking));
+    return METLDPC_OK;
+}
+
+metldpc_status host_stream(metldpc_decoder d, int32_t batch, int md, int32_t dim, float snr, const float* in_h,
+                           const float* xnorm_h, const uint32_t* synd_h, int N, uint32_t* bits_h, int32_t* iters_h,
+                           uint8_t* conv_h) {
+    const HostLayout& L = d->code->host;
+    const size_t n = size_t(L.n), W = size_t(L.m + 31) / 32, NW = size_t(L.n + 31) / 32;
+    const size_t nx = md ? n / size_t(dim) : 0;
+    const int cap = std::min(d->max_batch, kHostStreamCap);
+    metldpc_status st;
+    if ((st = ensure_host_streams(d))) return st;
+    auto& hs = d->hs;
+    if (!hs.llr) {
+        if ((st = dalloc(&hs.llr, size_t(cap) * n)) || (st = dalloc(&hs.synd, size_t(cap) * W)) ||
+            (st = dalloc(&hs.bits, size_t(cap) * NW)) || (st = dalloc(&hs.iters, size_t(cap))) ||
+            (st = dalloc(&hs.conv, size_t(cap))))
+            return st;
+    }
+    if (md && xnorm_h && hs.xnorm_cap < size_t(cap) * nx) {
+        dfree(hs.xnorm);
+        hs.xnorm_cap = 0;
+        if ((st = dalloc(&hs.xnorm, size_t(cap) * nx))) return st;
+        hs.xnorm_cap = size_t(cap) * nx;
+    }
+    const float c_md = md ? float(2.0 * std::sqrt(double(snr) * (1.0 + double(snr)))) : 0.f;
+    cudaError_t ce = cudaSuccess;
+    const char* what = "";
+    cudaEvent_t ev_job = nullptr, ev_first = nullptr, ev_free = nullptr;
+    HP(cudaEventCreateWithFlags(&ev_job, cudaEventDisableTiming));
+    HP(cudaEventCreateWithFlags(&ev_first, cudaEventDisableTiming));
+    HP(cudaEventCreateWithFlags(&ev_free, cudaEventDisableTiming));
+    for (int f0 = 0; f0 < batch && ce == cudaSuccess; f0 += cap) {
+        const int nb = std::min(cap, batch - f0);
+        // queue header first (avail = 0), then the copies may publish into it
+        if ((st = stream_setup(d, nb, hs.llr, hs.synd, N, hs.bits, hs.iters, hs.conv, 0, d->s_comp))) break;
+        HP(cudaEventRecord(ev_job, d->s_comp));
+        HP(cudaStreamWaitEvent(d->s_h2d, ev_job, 0));
+        for (int c0 = 0; c0 < nb && ce == cudaSuccess; c0 += kHostChunk) {
+            const int k = std::min(kHostChunk, nb - c0);
+            const size_t g0 = size_t(f0) + size_t(c0);
+            HP(cudaMemcpyAsync(hs.llr + size_t(c0) * n, in_h + g0 * n, size_t(k) * n * sizeof(float),
+                               cudaMemcpyHostToDevice, d->s_h2d));
+            if (md && xnorm_h)
+                HP(cudaMemcpyAsync(hs.xnorm + size_t(c0) * nx, xnorm_h + g0 * nx, size_t(k) * nx * sizeof(float),
+                                   cudaMemcpyHostToDevice, d->s_h2d));
+            HP(cudaMemcpyAsync(hs.synd + size_t(c0) * W, synd_h + g0 * W, size_t(k) * W * sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, d->s_h2d));
+            if (md && ce == cudaSuccess) {   // LLRs in place over the staged v (R13)
+                launch_md_llr(int64_t(k) * int64_t(n), int(n), dim, c_md, hs.llr + size_t(c0) * n,
+                              xnorm_h ? hs.xnorm + size_t(c0) * nx : nullptr, hs.llr + size_t(c0) * n, d->s_h2d);
+                HP(cudaGetLastError());
+                d->prof.launches++;
+            }
+            launch_publish(d->job, c0 + k, d->s_h2d);
+            HP(cudaGetLastError());
+            d->prof.launches++;
+            if (c0 == 0) HP(cudaEventRecord(ev_first, d->s_h2d));
+        }
+        if (ce != cudaSuccess) {
+            // never leave a launched queue waiting for frames that will not come
+            launch_publish(d->job, nb, d->s_h2d);
+            break;
+        }
+        HP(cudaStreamWaitEvent(d->s_comp, ev_first, 0));
+        if (ce != cudaSuccess) break;
+        if ((st = stream_launch(d, nb, d->s_comp))) break;
+        HP(cudaMemcpyAsync(bits_h + size_t(f0) * NW, hs.bits, size_t(nb) * NW * sizeof(uint32_t),
+                           cudaMemcpyDeviceToHost, d->s_comp));
+        HP(cudaMemcpyAsync(iters_h + f0, hs.iters, size_t(nb) * sizeof(int32_t), cudaMemcpyDeviceToHost, d->s_comp));
+        HP(cudaMemcpyAsync(conv_h + f0, hs.conv, size_t(nb), cudaMemcpyDeviceToHost, d->s_comp));
+        // the next super-chunk's copies overwrite the staging: after this one's decode and D2H
+        HP(cudaEventRecord(ev_free, d->s_comp));
+        HP(cudaStreamWaitEvent(d->s_h2d, ev_free, 0));
+    }
+    cudaError_t e1 = cudaStreamSynchronize(d->s_h2d);
+    cudaError_t e2 = cudaStreamSynchronize(d->s_comp);
+    if (ev_job) cudaEventDestroy(ev_job);
+    if (ev_first) cudaEventDestroy(ev_first);
+    if (ev_free) cudaEventDestroy(ev_free);
+    if (st) return st;
+    if (ce != cudaSuccess) return fail(METLDPC_ECUDA, std::string("host path: ") + what + ": " + cudaGetErrorString(ce));
+    if (e1 != cudaSuccess || e2 != cudaSuccess)
+        return fail(METLDPC_ECUDA, std::string("host path: ") + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+    return METLDPC_OK;
+}
+
 metldpc_status host_pipeline(metldpc_decoder d, int32_t batch, int md, int32_t dim, float snr, const float* in_h,
                              const float* xnorm_h, const uint32_t* synd_h, int32_t max_iter, uint32_t* bits_h,
                              int32_t* iters_h, uint8_t* conv_h) {
     const int N = max_iter ? max_iter : d->cfg.max_iter;
     cudaSetDevice(d->code->device);
+    if (stream_mode(d)) return host_stream(d, batch, md, dim, snr, in_h, xnorm_h, synd_h, N, bits_h, iters_h, conv_h);
     const HostLayout& L = d->code->host;
     const size_t n = size_t(L.n), W = size_t(L.m + 31) / 32, NW = size_t(L.n + 31) / 32, B = size_t(d->B);
     const size_t nx = md ? n / size_t(dim) : 0;
     const int K = d->K, S = 2 * K;
     metldpc_status st;
-    if (!d->s_comp) {
-        CUDA_TRY(cudaStreamCreateWithFlags(&d->s_h2d, cudaStreamNonBlocking));
-        CUDA_TRY(cudaStreamCreateWithFlags(&d->s_comp, cudaStreamNonBlocking));
-        CUDA_TRY(cudaStreamCreateWithFlags(&d->s_d2h, cudaStreamNonBlocking));
+    if ((st = ensure_host_streams(d))) return st;
+    if (d->st.empty()) {
         d->st.resize(size_t(S));
         for (auto& sl : d->st)
             if ((st = dalloc(&sl.llr, B * n)) || (st = dalloc(&sl.synd, B * W)) || (st = dalloc(&sl.bits, B * NW)) ||
-                (st = dalloc(&sl.iters, B)) || (st = dalloc(&sl.conv, B)) || (st = dalloc(&sl.xnorm, B * n / 8 + B)))
+                (st = dalloc(&sl.iters, B)) || (st = dalloc(&sl.conv, B)))
                 return st;
     }
-    float c_md = 0.f;
-    if (md) {
-        const double sd = double(snr);
-        c_md = float(2.0 * std::sqrt(sd * (1.0 + sd)));
+    if (md && xnorm_h && d->st_xnorm_cap < B * nx) {   // B * n / d floats per slot: sized for this call's d
+        for (auto& sl : d->st) {
+            dfree(sl.xnorm);
+            if ((st = dalloc(&sl.xnorm, B * nx))) {
+                d->st_xnorm_cap = 0;
+                return st;
+            }
+        }
+        d->st_xnorm_cap = B * nx;
     }
+    const float c_md = md ? float(2.0 * std::sqrt(double(snr) * (1.0 + double(snr)))) : 0.f;
+    cudaError_t ce = cudaSuccess;
+    const char* what = "";
     const size_t nslots = static_cast<size_t>(S);
-    std::vector<cudaEvent_t> in_ready(nslots), slot_free(nslots), out_ready(nslots), out_free(nslots);
-    for (int k = 0; k < S; ++k) {
-        cudaEventCreateWithFlags(&in_ready[size_t(k)], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&slot_free[size_t(k)], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&out_ready[size_t(k)], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&out_free[size_t(k)], cudaEventDisableTiming);
-        cudaEventRecord(slot_free[size_t(k)], d->s_comp);
-        cudaEventRecord(out_free[size_t(k)], d->s_d2h);
+    std::vector<cudaEvent_t> in_ready(nslots, nullptr), slot_free(nslots, nullptr), out_ready(nslots, nullptr),
+        out_free(nslots, nullptr);
+    for (size_t k = 0; k < nslots; ++k) {
+        HP(cudaEventCreateWithFlags(&in_ready[k], cudaEventDisableTiming));
+        HP(cudaEventCreateWithFlags(&slot_free[k], cudaEventDisableTiming));
+        HP(cudaEventCreateWithFlags(&out_ready[k], cudaEventDisableTiming));
+        HP(cudaEventCreateWithFlags(&out_free[k], cudaEventDisableTiming));
+        HP(cudaEventRecord(slot_free[k], d->s_comp));
+        HP(cudaEventRecord(out_free[k], d->s_d2h));
     }
     const int groups = (batch + d->B - 1) / d->B;
     st = METLDPC_OK;
+    auto stage_in = [&](int slot, int f0, int nb) {
+        auto& sl = d->st[size_t(slot)];
+        // the slot's previous decode and D2H must be done before new inputs overwrite it
+        HP(cudaStreamWaitEvent(d->s_h2d, slot_free[size_t(slot)], 0));
+        HP(cudaStreamWaitEvent(d->s_h2d, out_free[size_t(slot)], 0));
+        HP(cudaMemcpyAsync(sl.llr, in_h + size_t(f0) * n, size_t(nb) * n * sizeof(float), cudaMemcpyHostToDevice,
+                           d->s_h2d));
+        if (md && xnorm_h)
+            HP(cudaMemcpyAsync(sl.xnorm, xnorm_h + size_t(f0) * nx, size_t(nb) * nx * sizeof(float),
+                               cudaMemcpyHostToDevice, d->s_h2d));
+        HP(cudaMemcpyAsync(sl.synd, synd_h + size_t(f0) * W, size_t(nb) * W * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                           d->s_h2d));
+        if (md && ce == cudaSuccess) {   // LLRs in place over the staged v (metldpc_llr_from_md, R13)
+            launch_md_llr(int64_t(nb) * int64_t(n), int(n), dim, c_md, sl.llr, xnorm_h ? sl.xnorm : nullptr, sl.llr,
+                          d->s_h2d);
+            HP(cudaGetLastError());
+            d->prof.launches++;
+        }
+        HP(cudaEventRecord(in_ready[size_t(slot)], d->s_h2d));
+    };
+    auto stage_out = [&](int slot, int f0, int nb) {
+        auto& sl = d->st[size_t(slot)];
+        HP(cudaStreamWaitEvent(d->s_d2h, out_ready[size_t(slot)], 0));
+        HP(cudaMemcpyAsync(bits_h + size_t(f0) * NW, sl.bits, size_t(nb) * NW * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                           d->s_d2h));
+        HP(cudaMemcpyAsync(iters_h + f0, sl.iters, size_t(nb) * sizeof(int32_t), cudaMemcpyDeviceToHost, d->s_d2h));
+        HP(cudaMemcpyAsync(conv_h + f0, sl.conv, size_t(nb), cudaMemcpyDeviceToHost, d->s_d2h));
+        HP(cudaEventRecord(out_free[size_t(slot)], d->s_d2h));
+    };
     const bool queue = K > 1 && d->use_graph && !d->profiling;
     // Group queue (as in metldpc_decode): group gi uses staging slot gi mod 2K and workspace
     // gi mod K on that workspace's stream, ordered only by its own events (inputs staged,
     // previous occupant of the slot decoded and copied out) -- no per-round join.
-    for (int gi = 0; queue && gi < groups && st == METLDPC_OK; ++gi) {
+    for (int gi = 0; queue && gi < groups && st == METLDPC_OK && ce == cudaSuccess; ++gi) {
         const int k = gi % K, slot = gi % S;
         auto& sl = d->st[size_t(slot)];
         const int f0 = gi * d->B, nb = std::min(d->B, batch - f0);
         cudaStream_t gs = d->gs[size_t(k)];
-        cudaStreamWaitEvent(d->s_h2d, slot_free[size_t(slot)], 0);
-        cudaStreamWaitEvent(d->s_h2d, out_free[size_t(slot)], 0);
-        cudaMemcpyAsync(sl.llr, in_h + size_t(f0) * n, size_t(nb) * n * sizeof(float), cudaMemcpyHostToDevice, d->s_h2d);
-        if (md && xnorm_h)
-            cudaMemcpyAsync(sl.xnorm, xnorm_h + size_t(f0) * nx, size_t(nb) * nx * sizeof(float), cudaMemcpyHostToDevice,
-                            d->s_h2d);
-        cudaMemcpyAsync(sl.synd, synd_h + size_t(f0) * W, size_t(nb) * W * sizeof(uint32_t), cudaMemcpyHostToDevice,
-                        d->s_h2d);
-        if (md) {
-            launch_md_llr(int64_t(nb) * int64_t(n), int(n), dim, c_md, sl.llr, xnorm_h ? sl.xnorm : nullptr, sl.llr,
-                          d->s_h2d);
-            d->prof.launches++;
-        }
-        cudaEventRecord(in_ready[size_t(slot)], d->s_h2d);
-        cudaStreamWaitEvent(gs, in_ready[size_t(slot)], 0);
+        stage_in(slot, f0, nb);
+        HP(cudaStreamWaitEvent(gs, in_ready[size_t(slot)], 0));
+        if (ce != cudaSuccess) break;
         GroupJob j{k, sl.llr, sl.synd, nb, sl.bits, sl.iters, sl.conv, gs};
         if ((st = group_begin(d, j, N)) || (st = group_loop(d, j, N)) || (st = group_end(d, j, N))) break;
-        cudaEventRecord(out_ready[size_t(slot)], gs);
-        cudaEventRecord(slot_free[size_t(slot)], gs);
-        cudaStreamWaitEvent(d->s_d2h, out_ready[size_t(slot)], 0);
-        cudaMemcpyAsync(bits_h + size_t(f0) * NW, sl.bits, size_t(nb) * NW * sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                        d->s_d2h);
-        cudaMemcpyAsync(iters_h + f0, sl.iters, size_t(nb) * sizeof(int32_t), cudaMemcpyDeviceToHost, d->s_d2h);
-        cudaMemcpyAsync(conv_h + f0, sl.conv, size_t(nb), cudaMemcpyDeviceToHost, d->s_d2h);
-        cudaEventRecord(out_free[size_t(slot)], d->s_d2h);
+        HP(cudaEventRecord(out_ready[size_t(slot)], gs));
+        HP(cudaEventRecord(slot_free[size_t(slot)], gs));
+        stage_out(slot, f0, nb);
     }
-    if (queue)
-        for (int k = 0; k < K; ++k) cudaStreamSynchronize(d->gs[size_t(k)]);
-    for (int g0 = 0, round = 0; !queue && g0 < groups && st == METLDPC_OK; g0 += K, ++round) {
+    for (int g0 = 0, round = 0; !queue && g0 < groups && st == METLDPC_OK && ce == cudaSuccess; g0 += K, ++round) {
         std::vector<GroupJob> jobs;
         std::vector<int> slots;
         for (int k = 0; k < K && g0 + k < groups; ++k) {
             const int slot = (round & 1) * K + k;
             auto& sl = d->st[size_t(slot)];
             const int f0 = (g0 + k) * d->B, nb = std::min(d->B, batch - f0);
-            // the slot's previous D2H must be done before new inputs overwrite its outputs' neighbours
-            cudaStreamWaitEvent(d->s_h2d, slot_free[size_t(slot)], 0);
-            cudaStreamWaitEvent(d->s_h2d, out_free[size_t(slot)], 0);
-            cudaMemcpyAsync(sl.llr, in_h + size_t(f0) * n, size_t(nb) * n * sizeof(float), cudaMemcpyHostToDevice,
-                            d->s_h2d);
-            if (md && xnorm_h)
-                cudaMemcpyAsync(sl.xnorm, xnorm_h + size_t(f0) * nx, size_t(nb) * nx * sizeof(float),
-                                cudaMemcpyHostToDevice, d->s_h2d);
-            cudaMemcpyAsync(sl.synd, synd_h + size_t(f0) * W, size_t(nb) * W * sizeof(uint32_t), cudaMemcpyHostToDevice,
-                            d->s_h2d);
-            if (md) {   // LLRs in place over the staged v (metldpc_llr_from_md, R13), on the copy stream
-                launch_md_llr(int64_t(nb) * int64_t(n), int(n), dim, c_md, sl.llr, xnorm_h ? sl.xnorm : nullptr, sl.llr,
-                              d->s_h2d);
-                d->prof.launches++;
-            }
-            cudaEventRecord(in_ready[size_t(slot)], d->s_h2d);
+            stage_in(slot, f0, nb);
             GroupJob j{k, sl.llr, sl.synd, nb, sl.bits, sl.iters, sl.conv, d->s_comp};
             j.ready = in_ready[size_t(slot)];
             j.done = out_ready[size_t(slot)];
             jobs.push_back(j);
             slots.push_back(slot);
         }
-        st = decode_round(d, jobs, N, d->s_comp);
+        if (ce != cudaSuccess) break;
+        if ((st = decode_round(d, jobs, N, d->s_comp))) break;
         for (size_t q = 0; q < jobs.size(); ++q) {
-            const int slot = slots[q];
-            auto& sl = d->st[size_t(slot)];
-            const int f0 = (g0 + int(q)) * d->B, nb = jobs[q].nb;
-            cudaEventRecord(slot_free[size_t(slot)], d->s_comp);
-            cudaStreamWaitEvent(d->s_d2h, out_ready[size_t(slot)], 0);
-            cudaMemcpyAsync(bits_h + size_t(f0) * NW, sl.bits, size_t(nb) * NW * sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                            d->s_d2h);
-            cudaMemcpyAsync(iters_h + f0, sl.iters, size_t(nb) * sizeof(int32_t), cudaMemcpyDeviceToHost, d->s_d2h);
-            cudaMemcpyAsync(conv_h + f0, sl.conv, size_t(nb), cudaMemcpyDeviceToHost, d->s_d2h);
-            cudaEventRecord(out_free[size_t(slot)], d->s_d2h);
+            HP(cudaEventRecord(slot_free[size_t(slots[q])], d->s_comp));
+            stage_out(slots[q], (g0 + int(q)) * d->B, jobs[q].nb);
         }
     }
-    cudaError_t e = cudaStreamSynchronize(d->s_d2h);
+    cudaError_t e = cudaStreamSynchronize(d->s_h2d);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(d->s_d2h);
     if (e == cudaSuccess) e = cudaStreamSynchronize(d->s_comp);
-    for (int k = 0; k < S; ++k) {
-        cudaEventDestroy(in_ready[size_t(k)]);
-        cudaEventDestroy(slot_free[size_t(k)]);
-        cudaEventDestroy(out_ready[size_t(k)]);
-        cudaEventDestroy(out_free[size_t(k)]);
+    for (int k = 0; queue && k < K; ++k)
+        if (e == cudaSuccess) e = cudaStreamSynchronize(d->gs[size_t(k)]);
+    for (size_t k = 0; k < nslots; ++k) {
+        if (in_ready[k]) cudaEventDestroy(in_ready[k]);
+        if (slot_free[k]) cudaEventDestroy(slot_free[k]);
+        if (out_ready[k]) cudaEventDestroy(out_ready[k]);
+        if (out_free[k]) cudaEventDestroy(out_free[k]);
     }
     if (st) return st;
+    if (ce != cudaSuccess) return fail(METLDPC_ECUDA, std::string("host pipeline: ") + what + ": " + cudaGetErrorString(ce));
     if (e != cudaSuccess) return fail(METLDPC_ECUDA, std::string("host pipeline: ") + cudaGetErrorString(e));
     return METLDPC_OK;
 }
@@ -1089,6 +1238,28 @@ metldpc_status metldpc_debug_dump(metldpc_decoder d, int32_t lane, float* r_out,
     if (L_out && L.n_a)
         CUDA_TRY(cudaMemcpy2D(L_out, sizeof(float), d->ws[size_t(d->last_ws)].L + lane, 2 * size_t(d->B) * sizeof(float), sizeof(float),
                               size_t(L.n_a), cudaMemcpyDeviceToHost));
+    return METLDPC_OK;
+}
+
+metldpc_status metldpc_debug_step(metldpc_decoder d, int32_t k, uintptr_t stream) {
+    if (!d) return fail(METLDPC_EINVAL, "NULL decoder");
+    if (k < 1) return fail(METLDPC_EINVAL, "k must be >= 1");
+    if (d->last_nb < 1 || d->last_streaming)
+        return fail(METLDPC_EINVAL, "debug_step needs a preceding group-mode decode (lane_refill = 0 or early_term = 0)");
+    cudaSetDevice(d->code->device);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const CodeDev cd = code_dev(d->code, d->cfg.rule);
+    const Group g = group_of(d, d->last_ws);
+    // re-activate the group's valid lanes (the final latch retired them), then k plain
+    // iterations: CN classes (no syndrome test) + VN finish, exactly the decode's pass
+    launch_init_ctl(g, d->last_nb, d->cfg.max_iter, s);
+    for (int i = 1; i <= k; ++i) {
+        launch_cn_classes(d, cd, g, i, false, s, d->l2w[size_t(d->last_ws)]);
+        launch_finish(cd, g, d->vn_grid, s, d->l2w[size_t(d->last_ws)]);
+        d->prof.launches += int64_t(d->cn_classes.size()) + 1;
+    }
+    d->prof.launches++;
+    CUDA_TRY(cudaGetLastError());
     return METLDPC_OK;
 }
 

@@ -92,6 +92,11 @@ metldpc_status build_layout(int32_t n, int32_t m, int64_t E, const int64_t* cn_p
         L.max_vn_deg = std::max(L.max_vn_deg, deg[v]);
     }
     L.n_a = n_a;
+    // N3: the fixed-point VN sum of an active VN is exact only while deg * 30 * 2^17 stays
+    // inside the 32-bit accumulator (deg <= kMaxVnDeg)
+    if (L.max_vn_deg > kMaxVnDeg)
+        return fail(METLDPC_EUNSUPPORTED, "VN degree " + std::to_string(L.max_vn_deg) + " > " +
+                                              std::to_string(kMaxVnDeg) + " (fixed-point VN sum, DESIGN.md N3)");
     // canonical active-edge id: rank among active edges in the caller's CSR order
     std::vector<int32_t> canon(E, -1);
     int64_t tc = 0;

@@ -9,6 +9,8 @@
 namespace metldpc {
 
 constexpr int kMaxCnDeg = 32;          // templated CN kernel bound (metldpc.h: EUNSUPPORTED above)
+// DESIGN.md N3: deg * (2^22 + 30 * 2^17) < 2^32, so the biased fixed-point VN sum never wraps
+constexpr int kMaxVnDeg = 512;
 constexpr float kRMax = 30.0f;         // DESIGN.md R6
 // phi tables (N2): 2^J bins per binade on [2^-44, 2^6); EXACT J = 4 (cubic,
 // 4 floats/bin), PHI_LUT J = 5 (linear, 2 floats/bin).

@@ -708,17 +708,19 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND>::THREADS, 1)
             }
             mbar_wait(bar_a + 8 * st, ph);
             const float* sr = reinterpret_cast<const float*>(stage + st * PC::STG);
-            if (any_fresh) {   // r^0 = 0 for a lane whose frame starts in this pass (Step 2)
-                const bool f0 = (s_fresh[0] >> lane) & 1u, f1 = (s_fresh[1] >> lane) & 1u;
-#pragma unroll
-                for (int s = 0; s < NA; ++s) {
-                    if (f0) reinterpret_cast<float*>(stage + st * PC::STG)[s * 64 + lane] = 0.0f;
-                    if (f1) reinterpret_cast<float*>(stage + st * PC::STG)[s * 64 + 32 + lane] = 0.0f;
-                }
-            }
 #pragma unroll
             for (int s = 0; s < NA; ++s) {
                 r2[s] = make_float2(sr[s * 64 + lane], sr[s * 64 + 32 + lane]);
+            }
+            // r^0 = 0 for a lane whose frame starts in this pass (Step 2), applied in registers:
+            // the ring stages are written only by the TMA (async proxy), never by the threads
+            if (any_fresh) {
+                const bool f0 = (s_fresh[0] >> lane) & 1u, f1 = (s_fresh[1] >> lane) & 1u;
+#pragma unroll
+                for (int s = 0; s < NA; ++s) {
+                    if (f0) r2[s].x = 0.0f;
+                    if (f1) r2[s].y = 0.0f;
+                }
             }
             float2 lam = make_float2(0.0f, 0.0f);
             if constexpr (ND > 0) lam = make_float2(sr[NA * 64 + lane], sr[NA * 64 + 32 + lane]);
@@ -1229,12 +1231,15 @@ __global__ void k_latch_stream(Group g, StreamJob* job, cudaGraphConditionalHand
 
 // End of a streaming pass: advance the global pass counter; loop while any lane iterates
 // or waits for its refill wave.
-__global__ void k_stream_ctl(Group g, cudaGraphConditionalHandle while_h) {
+// (The pass cap only guards against a host-path queue that never fills: a correct run ends
+// long before it, when every frame has been decoded.)
+__global__ void k_stream_ctl(Group g, const StreamJob* job, cudaGraphConditionalHandle while_h) {
     *g.iter = *g.iter + 1;
-    g.stat[0] += 1u;
+    const uint32_t passes = g.stat[0] + 1u;
+    g.stat[0] = passes;
     uint32_t any = 0;
     for (int q = 0; q < g.C; ++q) any |= g.act[q] | g.fin[q];
-    cudaGraphSetConditional(while_h, any ? 1u : 0u);
+    cudaGraphSetConditional(while_h, (any && passes < uint32_t(job->max_passes)) ? 1u : 0u);
 }
 
 // Refill wave 1/4: outputs of the finished lanes (as k_finalize, per lane: frame lane_frame,
@@ -1271,9 +1276,12 @@ __global__ void __launch_bounds__(256) k_finalize_lanes(CodeDev cd, Group g, Str
     job->bits[size_t(f) * NW + wblk] = word;
 }
 
-// Refill wave 2/4: the finished lanes take the next frames of the queue (in lane order).
+// Refill wave 2/4: the finished lanes take the next frames of the queue (in lane order),
+// among those whose inputs are on the device (f < avail).  A freed lane that gets no frame
+// stays free (in `fin`, lane_frame = -1) while the queue still has frames to come, so a
+// later wave can fill it; once every frame is claimed it retires.
 __global__ void k_refill_assign(Group g, StreamJob* job) {
-    __shared__ int s_base;
+    __shared__ int s_base, s_take, s_pending;
     __shared__ uint32_t s_new[4];
     const int b = threadIdx.x, c = b >> 5, bit = b & 31;
     const bool freed = b < g.B && ((g.fin[c] >> bit) & 1u);
@@ -1284,21 +1292,38 @@ __global__ void k_refill_assign(Group g, StreamJob* job) {
         cnt += __popc(m);
     }
     if (freed) rank += __popc(g.fin[c] & ((1u << bit) - 1u));
-    if (b == 0) s_base = cnt ? atomicAdd(&job->next, int(cnt)) : 0;
+    if (b == 0) {
+        // claim up to cnt frames from [next, min(avail, nframes)) (one CAS loop per wave; the
+        // K workspaces of a decode share the queue)
+        const int nf = job->nframes;
+        const int avail = min(*reinterpret_cast<volatile int*>(&job->avail), nf);
+        int cur = *reinterpret_cast<volatile int*>(&job->next), take = 0;
+        while (cnt) {
+            take = min(int(cnt), avail - cur);
+            if (take <= 0) { take = 0; break; }
+            const int prev = atomicCAS(&job->next, cur, cur + take);
+            if (prev == cur) break;
+            cur = prev;
+        }
+        s_base = cur;
+        s_take = take;
+        s_pending = (cur + take) < nf;
+    }
     __syncthreads();
     const int f = s_base + int(rank);
-    const bool got = freed && f < job->nframes;
+    const bool got = freed && int(rank) < s_take;
     if (freed) {
         g.lane_frame[b] = got ? f : -1;
         g.lane_l[b] = got ? 1 : 0;
     }
     const uint32_t nb = __ballot_sync(FULL, got);
+    const uint32_t wait = __ballot_sync(FULL, freed && !got);
     if (bit == 0 && c < g.C) s_new[c] = nb;
     __syncthreads();
-    if (b < g.C) {
-        g.newm[b] = s_new[b];
-        g.fin[b] = 0u;
-        g.invalid[b] &= ~s_new[b];
+    if (b < g.C) g.newm[b] = s_new[b];
+    if (bit == 0 && c < g.C) {
+        g.fin[c] = s_pending ? wait : 0u;   // free lanes waiting for frames still to come
+        g.invalid[c] &= ~nb;
     }
 }
 
@@ -1315,7 +1340,7 @@ __global__ void __launch_bounds__(256) k_refill_scatter(CodeDev cd, Group g, Str
     for (int rr = w; rr < 32; rr += 8) {
         const int f = ((nm >> rr) & 1u) ? g.lane_frame[c * 32 + rr] : -1;
         const int i = i0 + lane;
-        tile[rr][lane] = (f >= 0 && i < cd.n) ? __ldcs(job->llr + size_t(f) * cd.n + i) : 0.0f;
+        tile[rr][lane] = (f >= 0 && i < cd.n) ? __ldcv(job->llr + size_t(f) * cd.n + i) : 0.0f;
     }
     __syncthreads();
     const size_t off = size_t(c) * 32 + lane;
@@ -1348,7 +1373,7 @@ __global__ void __launch_bounds__(256) k_refill_synd(CodeDev cd, Group g, Stream
     const uint32_t nm = g.newm[c];
     if (!nm) return;
     const int f = ((nm >> lane) & 1u) ? g.lane_frame[c * 32 + lane] : -1;
-    const uint32_t word = (f >= 0) ? __ldg(job->synd + size_t(f) * W + wd) : 0u;
+    const uint32_t word = (f >= 0) ? __ldcv(job->synd + size_t(f) * W + wd) : 0u;
     uint32_t mine = 0;
 #pragma unroll
     for (int bb = 0; bb < 32; ++bb) {
@@ -1387,16 +1412,17 @@ __global__ void k_refill_activate(Group g) {
 
 // ------------------------------------------------------------------ LLR from MD output (a1, R13)
 
-__global__ void __launch_bounds__(256) k_md_llr(int64_t total, int n, int d, float c, const float* __restrict__ v,
-                                                const float* __restrict__ xnorm, float* __restrict__ out,
-                                                float xd) {
+// v and out may alias (the host-buffer path converts the staged v in place), so neither is
+// __restrict__ and v is read through the coherent path.
+__global__ void __launch_bounds__(256) k_md_llr(int64_t total, int n, int d, float c, const float* v,
+                                                const float* __restrict__ xnorm, float* out, float xd) {
     const int nb = n / d;
     for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
         const int64_t f = e / n;
         const int i = int(e - f * n);
         const float xb = xnorm ? __ldg(xnorm + f * nb + i / d) : xd;
         const float cx = __fmul_rn(c, xb);
-        out[e] = __fmul_rn(cx, __ldg(v + e));
+        out[e] = __fmul_rn(cx, v[e]);
     }
 }
 
@@ -1652,9 +1678,18 @@ void launch_latch_stream(const Group& g, StreamJob* job, unsigned long long if_h
     launch_small(reinterpret_cast<void*>(&k_latch_stream), dim3(1), dim3(128), args, s, pdl);
 }
 
-void launch_stream_ctl(const Group& g, unsigned long long while_handle, cudaStream_t s) {
-    k_stream_ctl<<<1, 1, 0, s>>>(g, cudaGraphConditionalHandle(while_handle));
+void launch_stream_ctl(const Group& g, const StreamJob* job, unsigned long long while_handle, cudaStream_t s) {
+    k_stream_ctl<<<1, 1, 0, s>>>(g, job, cudaGraphConditionalHandle(while_handle));
 }
+
+// Host path: frames [0, avail) of the queue are on the device (launched on the copy stream
+// after their H2D copies and LLR conversion, so stream order makes the data visible first).
+__global__ void k_publish(StreamJob* job, int avail) {
+    __threadfence();
+    atomicMax(&job->avail, avail);
+}
+
+void launch_publish(StreamJob* job, int avail, cudaStream_t s) { k_publish<<<1, 1, 0, s>>>(job, avail); }
 
 void launch_refill_wave(const CodeDev& cd, const Group& g, StreamJob* job, cudaStream_t s) {
     const int NW = (cd.n + 31) / 32, W = (cd.m + 31) / 32;

@@ -48,9 +48,12 @@ struct StreamJob {
     int32_t* iters;        // [nframes]
     uint8_t* conv;         // [nframes]
     int32_t nframes;
-    int32_t next;          // atomically advanced by the refill waves
+    int32_t next;          // atomically advanced by the refill waves (frames claimed)
     int32_t N;             // max_iter
     int32_t wave_min;      // refill once this many lanes have finished (or none iterates)
+    int32_t avail;         // frames [0, avail) have their inputs on the device (host path:
+                           // raised chunk by chunk by k_publish on the copy stream)
+    int32_t max_passes;    // hang guard: a workspace's loop stops after this many passes
 };
 
 struct CodeDev {
@@ -94,8 +97,9 @@ void launch_loop_ctl(const Group& g, unsigned long long cond_handle, cudaStream_
 void launch_stream_init(const Group& g, cudaStream_t s);
 void launch_latch_stream(const Group& g, StreamJob* job, unsigned long long if_handle, cudaStream_t s,
                          bool pdl = false);
-void launch_stream_ctl(const Group& g, unsigned long long while_handle, cudaStream_t s);
+void launch_stream_ctl(const Group& g, const StreamJob* job, unsigned long long while_handle, cudaStream_t s);
 void launch_refill_wave(const CodeDev& cd, const Group& g, StreamJob* job, cudaStream_t s);
+void launch_publish(StreamJob* job, int avail, cudaStream_t s);
 // l >= 1: iteration given by the host; l == 0: read from Group::iter (graph body), with
 // et telling whether iterations >= 2 test the syndrome.
 void launch_cn(const CodeDev& cd, const Group& g, int rule, int D, int nd, int begin, int count, int ts, int grid,
