@@ -19,6 +19,7 @@ _LIB = _DIR / "liboracle_bp.so"
 RULE_EXACT = 0
 RULE_PHI_LUT = 1
 NO_SKIP = 0x100   # variant bit: iterate degree-1 VNs too (Table 1 "without skipping")
+MSG16 = 0x200     # fp32 (M3) variant bit: messages stored as rint(2^10 r) 2^-10 (R28/N7)
 R_MAX = 30.0
 
 _lib = None
@@ -134,9 +135,11 @@ def syndrome(code, bits: np.ndarray) -> np.ndarray:
 
 def decode(code, llr: np.ndarray, synd_words: np.ndarray, max_iter: int, early_term: bool = True,
            rule: int = RULE_EXACT, prec: int = 32, trace: bool = False, posterior: bool = False,
-           no_skip: bool = False):
+           no_skip: bool = False, msg16: bool = False):
     """Decode ONE frame.  prec=32 -> M3 (fp32 replay), prec=64 -> M2 (fp64 definition).
     no_skip iterates degree-1 VNs too (Table 1 "without skipping", R26).
+    msg16 (M3 only) stores the messages in 16 bits, rint(2^10 r) 2^-10 (DESIGN.md R28/N7);
+    r_trace then holds the stored messages.
 
     Returns dict(bits uint8[n], iters, converged, [r_trace, L_trace], [post]).
     """
@@ -151,6 +154,10 @@ def decode(code, llr: np.ndarray, synd_words: np.ndarray, max_iter: int, early_t
         E_it, n_a = graph_sizes(code, no_skip)
     if no_skip:
         rule = rule | NO_SKIP
+    if msg16:
+        if prec != 32:
+            raise ValueError("msg16 is an fp32 (M3) storage variant")
+        rule = rule | MSG16
     if prec == 32:
         lam = np.ascontiguousarray(llr, np.float32)
         if trace:

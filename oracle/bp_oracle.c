@@ -61,6 +61,15 @@ enum { RULE_EXACT = 0, RULE_PHI_LUT = 1 };
  * its CN input is the extrinsic L - r (R26). */
 #define ORC_NO_SKIP 0x100
 
+/* Variant bit of the fp32 decoder (M3) only: 16-bit message storage (R28 / N7).
+ * The paper fixes no precision for the stored messages and names global-memory access as
+ * the cost that dominates.  The CN output o of iteration l is kept for the next
+ * iteration as the integer rint(2^10 o) (round half to even; |o| <= R_MAX = 30 gives
+ * |rint(2^10 o)| <= 30720 < 2^15), i.e. the stored message is rint(2^10 o) * 2^-10, within
+ * 2^-11 of o.  The VN sum of Eq. (4)/(5) of iteration l is taken over the unrounded outputs
+ * o (N3); the extrinsic of iteration l + 1, x = L - r (R10), reads the stored message. */
+#define ORC_MSG16 0x200
+
 /* ------------------------------------------------------------------ phi */
 
 /* phi(y) = ln((e^y + 1)/(e^y - 1)) = -ln tanh(y/2); phi(0) = +inf, phi(inf) = 0. */
@@ -329,6 +338,11 @@ static void decide32(const graph_t* g, const float* L, const uint8_t* dec1, uint
         c[v] = (g->vn_act[v] >= 0) ? (L[g->vn_act[v]] < 0.0f) : dec1[v];
 }
 
+/* DESIGN.md N7: the stored copy of the messages under ORC_MSG16 (see above). */
+static void store_msg16(float* r, int64_t E_it) {
+    for (int64_t e = 0; e < E_it; ++e) r[e] = rintf(r[e] * 1024.0f) * (1.0f / 1024.0f);   /* both products exact */
+}
+
 static int all_finite32(const float* a, int n) {
     for (int i = 0; i < n; ++i) if (!isfinite(a[i])) return 0;
     return 1;
@@ -344,6 +358,7 @@ int orc_decode_f32(int rule, int n, int m, const int64_t* cn_ptr, const int32_t*
                    float* r_trace, float* L_trace) {
     graph_t g;
     int rc = graph_build(&g, n, m, cn_ptr, edge_vn, vn_ptr, vn_edge, rule);
+    const int msg16 = (rule & ORC_MSG16) != 0;
     rule &= 0xff;
     if (rc) { graph_free(&g); return rc; }
     memset(bits_out, 0, (size_t)n);
@@ -357,6 +372,7 @@ int orc_decode_f32(int rule, int n, int m, const int64_t* cn_ptr, const int32_t*
     for (int l = 1; l <= max_iter; ++l) {
         cn_phase32(&g, rule, lam, synd, r_old, L_old, r_new, dec1);
         vn_phase32(&g, lam, r_new, L_new);
+        if (msg16) store_msg16(r_new, g.E_it);   /* what iteration l + 1 reads (N7) */
         decide32(&g, L_new, dec1, bits_out);
         if (r_trace) memcpy(r_trace + (size_t)(l - 1) * g.E_it, r_new, (size_t)g.E_it * 4);
         if (L_trace) memcpy(L_trace + (size_t)(l - 1) * g.n_a, L_new, (size_t)g.n_a * 4);

@@ -424,3 +424,106 @@ def test_degree1_decision_unclamped():
         for rule in (bp.RULE_EXACT, bp.RULE_PHI_LUT):
             o = bp.decode(code, lam, pack_bits([0, 0]), 1, early_term=False, rule=rule, prec=prec)
             assert int(o["bits"][3]) == 0, (prec, rule)
+
+
+# ----------------------------------------------------------------- 16-bit message storage (R28 / N7)
+
+@pytest.mark.parametrize("rule", [bp.RULE_EXACT, bp.RULE_PHI_LUT])
+def test_msg16_teacher_forced_vs_m2(code_c1, rule):
+    """BASELINE north_star tolerance with 16-bit stored messages: from the M3-msg16
+    state (stored r^{l-1}, L^{l-1}) one fp64 step of the plain definition (M2) lands
+    within |dLLR| <= 1e-3 max(1, |LLR|) of the stored r^l and of L^l, every l, on
+    converging and non-converging frames (the storage rounding is <= 2^-11 < 1e-3)."""
+    for fid, snr in [(0, 0.161), (1, 0.3), (2, 0.22)]:
+        f = gen_frame(code_c1, snr, 2, fid)
+        lam32 = bp.llr_from_md_f32(f["v"], f["xnorm"], snr)
+        o = bp.decode(code_c1, lam32, f["synd"], 60, rule=rule, prec=32, trace=True, msg16=True)
+        E_it, n_a = bp.graph_sizes(code_c1)
+        r_prev = np.zeros(E_it)
+        act = np.diff(code_c1.vn_ptr) >= 2
+        L_prev = lam32.astype(np.float64)[act]
+        worst = 0.0
+        for l in range(o["iters"]):
+            r64, L64 = bp.step64(code_c1, lam32, f["synd"], r_prev, L_prev, rule=rule)
+            r16, L32 = o["r_trace"][l].astype(np.float64), o["L_trace"][l].astype(np.float64)
+            dr = np.abs(r64 - r16) / np.maximum(1, np.abs(r64))
+            assert (dr <= 1e-3).all(), (l, dr.max())
+            assert (np.abs(L64 - L32) <= 1e-3 * np.maximum(1, np.abs(L64))).all(), l
+            worst = max(worst, dr.max())
+            r_prev, L_prev = r16, L32
+        assert worst > 1e-4   # the rounding is visible (a stored fp32 copy would sit near 1e-6)
+
+
+def test_msg16_storage_grid_and_first_iteration(code_c1):
+    """N7: every stored message is an integer multiple of 2^-10 of magnitude <= 30 and
+    lies within 2^-11 of the fp32 decoder's message at l = 1 (identical inputs x = lambda
+    there); the posterior of l = 1 is the fp32 decoder's exactly, because the VN sum is
+    taken over the unrounded outputs (Eq. (4) of the current iteration)."""
+    f = gen_frame(code_c1, 0.161, 5, 0)
+    lam = bp.llr_from_md_f32(f["v"], f["xnorm"], 0.161)
+    a = bp.decode(code_c1, lam, f["synd"], 5, early_term=False, prec=32, trace=True)
+    b = bp.decode(code_c1, lam, f["synd"], 5, early_term=False, prec=32, trace=True, msg16=True)
+    q = b["r_trace"].astype(np.float64) * 1024.0
+    assert (q == np.round(q)).all() and (np.abs(q) <= 30720).all()
+    assert (np.abs(b["r_trace"][0].astype(np.float64) - a["r_trace"][0]) <= 2.0 ** -11).all()
+    assert np.array_equal(a["L_trace"][0], b["L_trace"][0])
+    assert not np.array_equal(a["r_trace"][0], b["r_trace"][0])
+
+
+@pytest.mark.parametrize("rule", [bp.RULE_EXACT, bp.RULE_PHI_LUT])
+def test_msg16_coset_translation_symmetry_bit_exact(code_c1, rule):
+    """The coset-translation symmetry (pins R1) survives the storage rounding: rint is
+    odd-symmetric (ties to even), so flipping lambda's signs on a coset translate flips
+    the stored messages exactly."""
+    from synth.frames import unpack_bits
+    rng = np.random.default_rng(4)
+    for fid, snr in [(0, 0.161), (1, 0.3)]:
+        f = gen_frame(code_c1, snr, 6, fid)
+        lam = bp.llr_from_md_f32(f["v"], f["xnorm"], snr)
+        e = rng.integers(0, 2, code_c1.n).astype(np.uint8)
+        s0 = unpack_bits(f["synd"], code_c1.m)
+        a = bp.decode(code_c1, lam, f["synd"], 40, rule=rule, prec=32, trace=True, msg16=True)
+        b = bp.decode(code_c1, (lam * (1 - 2.0 * e)).astype(np.float32), pack_bits(s0 ^ bp.syndrome(code_c1, e)),
+                      40, rule=rule, prec=32, trace=True, msg16=True)
+        assert a["iters"] == b["iters"] and a["converged"] == b["converged"]
+        assert ((a["bits"] ^ e) == b["bits"]).all()
+        assert np.array_equal(np.abs(a["r_trace"]), np.abs(b["r_trace"]))
+
+
+def test_msg16_zero_noise_and_tree_map():
+    """Noiseless input converges at l = 1 with c = u; on cycle-free codes the
+    decisions equal the brute-force bitwise MAP decisions (BP exact on trees) wherever
+    |MAP LLR| is clear of the storage rounding."""
+    from synth.codes import make_met_code
+    code = make_met_code("r0.1", 2048)
+    f = gen_frame(code, 0.161, 9, 1)
+    lam = ((1.0 - 2.0 * f["u"].astype(np.float64)) * 8.0).astype(np.float32)
+    o = bp.decode(code, lam, f["synd"], 100, prec=32, msg16=True)
+    assert o["converged"] and o["iters"] == 1 and (o["bits"] == f["u"]).all()
+    for seed in range(8):
+        rng = np.random.default_rng(500 + seed)
+        tc = tree_code(rng, n_cn=int(rng.integers(2, 6)))
+        lam = rng.normal(0.4, 1.5, tc.n).astype(np.float32)
+        s = rng.integers(0, 2, tc.m)
+        ref = brute.bitwise_map(tc.dense(), s, lam.astype(np.float64))
+        for rule in (bp.RULE_EXACT, bp.RULE_PHI_LUT):
+            o3 = bp.decode(tc, lam, pack_bits(s), 2 * tc.m + 2, early_term=False, prec=32, rule=rule, msg16=True)
+            clear = np.abs(ref) > 2e-2
+            assert (o3["bits"][clear] == (ref[clear] < 0)).all()
+
+
+def test_msg16_decodes_like_fp32_storage(code_c1):
+    """Converging frames decode to u with 16-bit storage as with fp32 storage, in about
+    the same number of iterations (the rounding is far below the channel noise)."""
+    n_ok, d_it = 0, []
+    for fid in range(8):
+        f = gen_frame(code_c1, 0.35, 7, fid)
+        lam = bp.llr_from_md_f32(f["v"], f["xnorm"], 0.35)
+        a = bp.decode(code_c1, lam, f["synd"], 100, prec=32)
+        b = bp.decode(code_c1, lam, f["synd"], 100, prec=32, msg16=True)
+        assert a["converged"] == b["converged"]
+        if b["converged"]:
+            n_ok += 1
+            assert (b["bits"] == f["u"]).all()
+            d_it.append(abs(a["iters"] - b["iters"]))
+    assert n_ok >= 6 and max(d_it) <= 2
