@@ -70,6 +70,8 @@ def parse():
     ap.add_argument("--no-skip", action="store_true",
                     help="iterate degree-1 VNs too (Table 1 'without skipping', METLDPC_CODE_NO_SKIP)")
     ap.add_argument("--lanes", type=int, default=64)
+    ap.add_argument("--msg-bits", type=int, choices=[32, 16], default=32,
+                    help="edge-message storage: fp32 or 16-bit rint(2^10 r) (DESIGN.md R28/N7)")
     ap.add_argument("--groups", type=int, default=1, help="lane groups decoded concurrently per GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -115,13 +117,14 @@ def oracle_throughput(a, code, v, xn, synd, budget_s: float, threads: int | None
     T = threads or max(1, min(host_cores(), 32, len(v)))
     lam = [bp.llr_from_md_f32(v[i % len(v)], xn[i % len(v)], a.snr) for i in range(T)]
     t0 = time.perf_counter()
-    bp.decode(code, lam[0], synd[0], 1, early_term=not a.no_et, rule=_rule(a), prec=32, no_skip=a.no_skip)
+    bp.decode(code, lam[0], synd[0], 1, early_term=not a.no_et, rule=_rule(a), prec=32, no_skip=a.no_skip,
+              msg16=a.msg_bits == 16)
     t_iter = max(time.perf_counter() - t0, 1e-3)
     I = int(max(1, min(a.iters, budget_s / t_iter)))
 
     def one(i):
         return bp.decode(code, lam[i], synd[i % len(synd)], I, early_term=not a.no_et, rule=_rule(a), prec=32,
-                         no_skip=a.no_skip)
+                         no_skip=a.no_skip, msg16=a.msg_bits == 16)
 
     t0 = time.perf_counter()
     with ThreadPoolExecutor(T) as ex:
@@ -187,7 +190,8 @@ def workload_name(a) -> str:
     return (f"{tag}: MET-LDPC {a.family} stand-in n={a.n}, SNR {a.snr}, max {a.iters} iterations "
             f"{'fixed' if a.no_et else 'with per-frame syndrome early termination'}, "
             f"{a.frames} frames/GPU per step, 8-D MD LLR input"
-            f"{', degree-1 VNs iterated (no skip)' if a.no_skip else ''}")
+            f"{', degree-1 VNs iterated (no skip)' if a.no_skip else ''}"
+            f"{', 16-bit edge messages' if a.msg_bits == 16 else ''}")
 
 
 def run_reference(a, rank: int, world: int):
@@ -348,7 +352,7 @@ def main():
     hc = B.Code(code, device=local, no_skip=a.no_skip)
     st = dict(st, iter_edges=hc.info.iter_edges, n_deg1=hc.info.n_deg1, n_active=hc.info.n_active)
     dec = B.Decoder(hc, F, rule=_rule(a), max_iter=a.iters, early_term=not a.no_et, lanes_per_group=a.lanes,
-                    groups_in_flight=a.groups, lane_refill=not a.no_refill)
+                    groups_in_flight=a.groups, lane_refill=not a.no_refill, msg_bits=a.msg_bits)
     llr = torch.empty_like(v)
     nw = (a.n + 31) // 32
     bits = torch.empty((F, nw), dtype=torch.int32, device=dev)
@@ -405,7 +409,7 @@ def main():
     # and kernels of different groups must not overlap, so the kernel durations come from an
     # isolated pass: one 64-lane group in flight, same data, same process.
     iso = B.Decoder(hc, min(F, a.lanes), rule=_rule(a), max_iter=a.iters, early_term=not a.no_et,
-                    lanes_per_group=a.lanes, groups_in_flight=1)
+                    lanes_per_group=a.lanes, groups_in_flight=1, msg_bits=a.msg_bits)
     Fi = min(F, a.lanes)
     outi = (bits[:Fi], iters[:Fi], conv[:Fi])
     iso.decode(llr[:Fi], sy[:Fi], out=outi)
@@ -418,7 +422,7 @@ def main():
     prof_k = iso.profile()
     iso.close()
     kernel_timing = "isolated pass: one 64-lane group in flight, CUDA events on the launch stream"
-    bm = metrics.bytes_per_cw_iter(st["iter_edges"], st["n_deg1"], st["n_active"], st["m"])
+    bm = metrics.bytes_per_cw_iter(st["iter_edges"], st["n_deg1"], st["n_active"], st["m"], s_r=a.msg_bits // 8)
     peak, peak_src = measured_peak_gbs()
     cn_gbs = prof_k["cn_lane_iters"] * bm["cn"] / (prof_k["cn_ms"] / 1e3) / 1e9 if prof_k["cn_ms"] > 0 else None
     # ncu DRAM bytes of the CN phase, captured for one workload (profiles/cn_traffic.json):
@@ -429,8 +433,8 @@ def main():
         try:
             tj = json.loads(tpath.read_text())
             w = tj.get("workload", {})
-            if (w.get("family"), w.get("n"), w.get("no_skip", False), w.get("lanes", 64), w.get("rule", "exact")) == \
-                    (a.family, a.n, bool(a.no_skip), a.lanes, a.rule):
+            if (w.get("family"), w.get("n"), w.get("no_skip", False), w.get("lanes", 64), w.get("rule", "exact"),
+                    w.get("msg_bits", 32)) == (a.family, a.n, bool(a.no_skip), a.lanes, a.rule, a.msg_bits):
                 traffic = tj.get("dram_bytes_per_launch")
                 pg = tj.get("production_graph", {})
                 traffic_prod = pg.get("dram_bytes_per_pass")
@@ -448,8 +452,8 @@ def main():
                                             if isinstance(traffic_prod, dict) and peak else traffic_prod),
                 "kernel": "CN phase: k_cn_pipe + k_cn_tile launches of one iteration (all degree classes, VN sums fused)",
                 "bytes_per_launch": bm["cn"] * min(F, a.lanes),
-                "bytes_model": "s(2 E_it + n_1 + n_a) + m/8 per codeword-iteration (SURVEY 8(d) without the "
-                               "VN write-back, which the fused VN sum keeps in L2), x 64 lanes",
+                "bytes_model": f"2 E_it s_r + 4 (n_1 + n_a) + m/8 per codeword-iteration, s_r = {a.msg_bits // 8} "
+                               "(SURVEY 8(d) without the VN write-back, which the fused VN sum keeps in L2), x 64 lanes",
                 "peak_source": peak_src,
                 "avg_launch_ms": prof_k["cn_ms"] / max(1, prof_k["cn_launches"]), "kernel_timing": kernel_timing,
                 "finish_avg_launch_ms": prof_k["vn_ms"] / max(1, prof_k["vn_launches"]),
@@ -500,6 +504,7 @@ def main():
                        "beta": metrics.beta(R, a.snr), "max_iter": a.iters, "early_term": not a.no_et,
                        "rule": a.rule.upper(), "frames_per_gpu": F, "distinct_frames_per_gpu": ND,
                        "lanes_per_group": a.lanes, "groups_in_flight": a.groups, "global_batch": F * world,
+                       "msg_bits": a.msg_bits,
                        "lane_refill": not a.no_refill,
                        "l2": "inputs larger than L2 (v 1 GB, edge messages 740 MB per 64-lane group)",
                        "parallelism": f"dp{world} (frames sharded f mod G; per-step NCCL all-reduce of the FER "

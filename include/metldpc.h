@@ -73,6 +73,11 @@ typedef struct {
                                   results are identical to group mode.  Default 1 (used by
                                   metldpc_decode when early_term and lanes_per_group = 64;
                                   the host-buffer calls and profiling use group mode).     */
+    int32_t msg_bits;          /* storage width of the edge messages r between iterations:
+                                  32 (fp32, default) or 16 (R28 / N7: rint(2^10 r)
+                                  in 16 bits, within 2^-11 of the CN output, which the VN sum
+                                  of the same iteration uses unrounded; halves the dominant
+                                  HBM stream).  16 needs lanes_per_group = 64.         */
 } metldpc_config_t;
 
 typedef struct {

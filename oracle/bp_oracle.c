@@ -340,7 +340,8 @@ static void decide32(const graph_t* g, const float* L, const uint8_t* dec1, uint
 
 /* DESIGN.md N7: the stored copy of the messages under ORC_MSG16 (see above). */
 static void store_msg16(float* r, int64_t E_it) {
-    for (int64_t e = 0; e < E_it; ++e) r[e] = rintf(r[e] * 1024.0f) * (1.0f / 1024.0f);   /* both products exact */
+    /* the integer q = rint(2^10 r) is what is stored (q = 0 reads back as +0); both products exact */
+    for (int64_t e = 0; e < E_it; ++e) r[e] = (float)(int32_t)rintf(r[e] * 1024.0f) * (1.0f / 1024.0f);
 }
 
 static int all_finite32(const float* a, int n) {

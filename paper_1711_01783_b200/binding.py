@@ -34,7 +34,8 @@ class MetLdpcError(RuntimeError):
 
 class Config(C.Structure):
     _fields_ = [("rule", C.c_int32), ("max_iter", C.c_int32), ("early_term", C.c_int32),
-                ("lanes_per_group", C.c_int32), ("groups_in_flight", C.c_int32), ("lane_refill", C.c_int32)]
+                ("lanes_per_group", C.c_int32), ("groups_in_flight", C.c_int32), ("lane_refill", C.c_int32),
+                ("msg_bits", C.c_int32)]
 
 
 class CodeInfo(C.Structure):
@@ -287,8 +288,9 @@ class Decoder:
 
     def __init__(self, code: Code, max_batch: int, rule: int = RULE_EXACT, max_iter: int = 100,
                  early_term: bool = True, lanes_per_group: int = 64, groups_in_flight: int | None = None,
-                 lane_refill: bool | None = None):
+                 lane_refill: bool | None = None, msg_bits: int = 32):
         cfg = metldpc_config_default()
+        cfg.msg_bits = msg_bits
         cfg.rule, cfg.max_iter, cfg.early_term, cfg.lanes_per_group = rule, max_iter, int(early_term), lanes_per_group
         if groups_in_flight is not None:
             cfg.groups_in_flight = groups_in_flight

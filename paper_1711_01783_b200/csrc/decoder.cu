@@ -144,6 +144,7 @@ Group group_of(metldpc_decoder d, int k) {
     Group g;
     g.B = d->B;
     g.C = d->C;
+    g.msg16 = d->cfg.msg_bits == 16 ? 1 : 0;
     g.r = w.r;
     g.L = w.L;
     g.lam_a = w.lam_a;
@@ -274,8 +275,10 @@ metldpc_status group_begin(metldpc_decoder d, const GroupJob& j, int N) {
     const CodeDev cd = code_dev(d->code, d->cfg.rule);
     const Group g = group_of(d, j.k);
     CUDA_TRY(cudaMemsetAsync(d->ws[size_t(j.k)].ctl + 8, 0, 4 * sizeof(uint32_t), j.s));
-    // r^0 = 0 (Step 2): the CN kernels read r unconditionally (~0.2 % of a decode's traffic)
-    CUDA_TRY(cudaMemsetAsync(g.r, 0, size_t(cd.E_it) * size_t(g.B) * sizeof(float), j.s));
+    // r^0 = 0 (Step 2): the CN kernels read r unconditionally (~0.2 % of a decode's traffic);
+    // a 16-bit row stores the message 0 as the half-word 0x8080 (N7, kernels.cu msg16_q)
+    if (g.msg16) CUDA_TRY(cudaMemsetAsync(g.r, 0x80, size_t(cd.E_it) * size_t(g.B) * 2, j.s));
+    else CUDA_TRY(cudaMemsetAsync(g.r, 0, size_t(cd.E_it) * size_t(g.B) * sizeof(float), j.s));
     launch_scatter(cd, g, j.llr, j.nb, j.s);
     launch_pack_syndrome(cd, g, j.synd, j.nb, j.s);
     launch_init_ctl(g, j.nb, N, j.s);
@@ -651,6 +654,7 @@ void metldpc_config_default(metldpc_config_t* cfg) {
     cfg->lanes_per_group = 64;
     cfg->groups_in_flight = 1;
     cfg->lane_refill = 1;
+    cfg->msg_bits = 32;
 }
 
 metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, const metldpc_config_t* cfg_in,
@@ -666,6 +670,9 @@ metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, cons
         return fail(METLDPC_EINVAL, "lanes_per_group must be 32, 64 or 128");
     if (cfg.groups_in_flight < 1 || cfg.groups_in_flight > 8) return fail(METLDPC_EINVAL, "groups_in_flight must be 1..8");
     if (max_batch < 1) return fail(METLDPC_EINVAL, "max_batch must be >= 1");
+    if (cfg.msg_bits != 32 && cfg.msg_bits != 16) return fail(METLDPC_EINVAL, "msg_bits must be 32 or 16");
+    if (cfg.msg_bits == 16 && cfg.lanes_per_group != 64)
+        return fail(METLDPC_EUNSUPPORTED, "msg_bits = 16 needs lanes_per_group = 64");
     if ((code->host.E_it + 1) * int64_t(cfg.lanes_per_group) >= (int64_t(1) << 31) ||
         (int64_t(code->host.n_a) + 1) * cfg.lanes_per_group >= (int64_t(1) << 31))
         return fail(METLDPC_EUNSUPPORTED, "edge-message array exceeds 2^31 elements per lane group");
@@ -684,7 +691,7 @@ metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, cons
     d->K = std::max(1, std::min(cfg.groups_in_flight, (max_batch + d->B - 1) / d->B));
     d->ws.resize(size_t(d->K));
     for (auto& w : d->ws) {
-        if ((s = dalloc(&w.r, size_t(L.E_it) * B)) || (s = dalloc(&w.L, 2 * size_t(L.n_a) * B)) ||
+        if ((s = dalloc(&w.r, size_t(L.E_it) * B * size_t(cfg.msg_bits) / 32)) || (s = dalloc(&w.L, 2 * size_t(L.n_a) * B)) ||
             (s = dalloc(&w.lam_a, size_t(L.n_a) * B)) || (s = dalloc(&w.lam1, size_t(L.n_1) * B)) ||
             (s = dalloc(&w.d1bits, 2 * size_t(L.n_1) * C)) || (s = dalloc(&w.synd_t, size_t(L.m) * C)) ||
             (s = dalloc(&w.ctl, 32)) || (s = dalloc(&w.iters, B)) || (s = dalloc(&w.conv, B)) ||
@@ -760,7 +767,8 @@ metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, cons
             ts = int(std::max(1L, std::min(long(cn_tile_max(D, k.nd)), want)));
             units = ((long(k.count) + ts - 1) / ts) * cn_units_per_tile(D, k.nd);
         }
-        const long full = long(sms) * std::max(1, cn_blocks_per_sm(cfg.rule, D, k.nd) / grid_split(d->K));
+        const long full =
+            long(sms) * std::max(1, cn_blocks_per_sm(cfg.rule, D, k.nd, cfg.msg_bits == 16) / grid_split(d->K));
         const long need = (units + warps_per_cta - 1) / warps_per_cta;
         d->cn_classes.push_back({D, k.nd, k.begin, k.count, ts, int(std::max(1L, std::min(full, need)))});
     }
@@ -1229,7 +1237,13 @@ metldpc_status metldpc_debug_dump(metldpc_decoder d, int32_t lane, float* r_out,
     cudaSetDevice(d->code->device);
     CUDA_TRY(cudaDeviceSynchronize());
     const HostLayout& L = d->code->host;
-    if (r_out && L.E_it) {   // device order (relabelled CNs) -> canonical active-edge CSR order
+    if (r_out && L.E_it && d->cfg.msg_bits == 16) {   // 16-bit rows (N7): half-word (lane & 31, lane >> 5)
+        std::vector<uint16_t> tmp(size_t(L.E_it));
+        const char* base = reinterpret_cast<const char*>(d->ws[size_t(d->last_ws)].r) + 4 * (lane & 31) + 2 * (lane >> 5);
+        CUDA_TRY(cudaMemcpy2D(tmp.data(), 2, base, 128, 2, size_t(L.E_it), cudaMemcpyDeviceToHost));
+        for (int64_t t = 0; t < L.E_it; ++t)
+            r_out[L.perm_r[size_t(t)]] = float(int(tmp[size_t(t)]) - 0x8080) * (1.0f / 1024.0f);
+    } else if (r_out && L.E_it) {   // device order (relabelled CNs) -> canonical active-edge CSR order
         std::vector<float> tmp(size_t(L.E_it));
         CUDA_TRY(cudaMemcpy2D(tmp.data(), sizeof(float), d->ws[size_t(d->last_ws)].r + lane, size_t(d->B) * sizeof(float), sizeof(float),
                               size_t(L.E_it), cudaMemcpyDeviceToHost));

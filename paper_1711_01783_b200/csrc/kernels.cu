@@ -307,11 +307,36 @@ __device__ __forceinline__ float2 phi_pair(uint32_t tabk, float y0, float y1, ui
 
 // DESIGN.md N1 for one CN and the two lanes (l, l + 32) of a thread, element-wise
 // identical to cn_lane (same fp32 operations, pairs where the two lanes do the same op).
-template <int RULE, int NA, int ND>
+// 16-bit message storage (R28 / N7), the two lanes of a thread in one 32-bit word
+// (lane l in the low half, lane l + 32 in the high half).  A stored half-word is w = q + 0x8080
+// for the message q * 2^-10, q = rint(2^10 o): fmaf(o, 2^10, 2^23 + 0x8080) = 2^23 + w exactly
+// (|q| <= 30720), so w is the low half of its bit pattern, and byte-filling a row with 0x80
+// stores q = 0 (r^0 = 0, Step 2).  Read back: PRMT puts w under the exponent of 2^23, one
+// exact FADD2 removes 2^23 + 0x8080.
+constexpr float kMsg16Magic = 8421504.0f;   // 2^23 + 0x8080
+__device__ __forceinline__ float2 msg16_q(uint32_t w) {
+    uint32_t a, b;
+    const uint32_t e = 0x4B000000u;   // bits of 2^23
+    asm("prmt.b32 %0, %1, %2, 0x7610;" : "=r"(a) : "r"(w), "r"(e));
+    asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(b) : "r"(w), "r"(e));
+    return f2sub(make_float2(__uint_as_float(a), __uint_as_float(b)), make_float2(kMsg16Magic, kMsg16Magic));
+}
+__device__ __forceinline__ uint32_t msg16_pack(float2 o) {
+    const float2 f = f2fma(o, make_float2(1024.0f, 1024.0f), make_float2(kMsg16Magic, kMsg16Magic));
+    uint32_t w;
+    asm("prmt.b32 %0, %1, %2, 0x5410;" : "=r"(w) : "r"(__float_as_uint(f.x)), "r"(__float_as_uint(f.y)));
+    return w;
+}
+
+// MSG = 0: r rows of fp32 (pr: float row pointer, ro: the messages).  MSG = 1: 16-bit rows
+// (pr: the thread's word of the row as uint32_t*, ro: the integers q of the stored messages,
+// x = fmaf(q, -2^-10, L) = the single rounding of L - q 2^-10, N7).
+template <int RULE, int NA, int ND, int MSG = 0>
 __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 0 ? NA : 1],
                                          const float2 (&ro)[NA > 0 ? NA : 1], float2 lam, uint2 sbit, uint2 d1prev,
-                                         float* pr, float* pla, const uint32_t (&offs)[NA > 0 ? NA : 1],
+                                         void* prv, float* pla, const uint32_t (&offs)[NA > 0 ? NA : 1],
                                          uint2& d1bit) {
+    float* pr = static_cast<float*>(prv);
     constexpr int D = NA + ND;
     const uint32_t one = one_bits();
     const float2 zero2 = make_float2(0.0f, 0.0f);
@@ -321,7 +346,8 @@ __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 
     uint32_t chk0 = sbit.x ^ d1prev.x, chk1 = sbit.y ^ d1prev.y;
 #pragma unroll
     for (int s = 0; s < NA; ++s) {
-        const float2 x = f2sub(Lv[s], ro[s]);                             // extrinsic q = L - r (R10)
+        const float2 x = MSG ? f2fma(ro[s], make_float2(-0.0009765625f, -0.0009765625f), Lv[s])
+                             : f2sub(Lv[s], ro[s]);                       // extrinsic q = L - r (R10)
         // [L < 0] and [x < 0] are the sign bits: L and x are never -0 (see k_scatter)
         chk0 ^= __float_as_uint(Lv[s].x) >> 31;
         chk1 ^= __float_as_uint(Lv[s].y) >> 31;
@@ -363,10 +389,16 @@ __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 
             // full 256-byte rows avoid partial-sector writes.
             const float2 fx = f2fma(o, make_float2(131072.0f, 131072.0f), make_float2(12582912.0f, 12582912.0f));
             unsigned int* pa = reinterpret_cast<unsigned int*>(pla + offs[s] + 64);
-            __stcs(pr + s * 64, o.x);
-            atomicAdd(pa, __float_as_uint(fx.x));              // VN sum (Eq. 4, N3)
-            __stcs(pr + s * 64 + 32, o.y);
-            atomicAdd(pa + 32, __float_as_uint(fx.y));
+            if constexpr (MSG) {
+                __stcs(reinterpret_cast<unsigned int*>(prv) + s * 32, msg16_pack(o));   // stored message (N7)
+                atomicAdd(pa, __float_as_uint(fx.x));              // VN sum of the unrounded o (Eq. 4, N3)
+                atomicAdd(pa + 32, __float_as_uint(fx.y));
+            } else {
+                __stcs(pr + s * 64, o.x);
+                atomicAdd(pa, __float_as_uint(fx.x));              // VN sum (Eq. 4, N3)
+                __stcs(pr + s * 64 + 32, o.y);
+                atomicAdd(pa + 32, __float_as_uint(fx.y));
+            }
         }
         if (s > 0) Q = f2add(Q, p[s]);
     }
@@ -391,11 +423,12 @@ __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 
 template <int NA>
 __host__ __device__ constexpr int cn_tile_min_blocks() { return NA <= 4 ? 2 : 1; }   // NA > 4: 128 registers
 
-template <int RULE, int NA, int ND>
+template <int RULE, int NA, int ND, int MSG = 0>
 __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_tile(CodeDev cd, Group g, CnCtl karg,
                                                                                   int begin, int count, int ts) {
     using PT = PhiT<RULE>;
     constexpr int LPT = (NA <= METLDPC_PAIR_MAX_NA) ? 2 : 1;     // lanes per thread
+    static_assert(!MSG || (LPT == 2 && METLDPC_CN_PAIR), "16-bit rows: two lanes per thread, pair path");
     constexpr int UPT = 2 / LPT;               // units per tile
     constexpr int NAS = NA > 0 ? NA : 1;
     constexpr int STAGE = (NA <= 4 ? 32 : 8) * NAS;
@@ -461,9 +494,15 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
                     const int o = idx[s];
                     if constexpr (NA <= 4 || LPT == 2) offs[s] = uint32_t(o) + lo;
 #pragma unroll
-                    for (int h = 0; h < LPT; ++h) {
+                    for (int h = 0; h < LPT; ++h)
                         Lv[h][s] = (NA <= 4) ? __ldg(g.L + offs[s] + h * 32) : __ldg(pL + o + h * 32);
-                        ro[h][s] = __ldcs(pr + s * 64 + h * 32);   // r^0 = 0: zeroed at group begin
+                    if constexpr (MSG) {   // 16-bit row: the thread's word holds lanes lane, lane + 32 (N7)
+                        const float2 q = msg16_q(__ldcs(reinterpret_cast<const unsigned int*>(g.r) + size_t(ab + s) * 32 + lane));
+                        ro[0][s] = q.x;
+                        ro[LPT - 1][s] = q.y;
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < LPT; ++h) ro[h][s] = __ldcs(pr + s * 64 + h * 32);   // r^0 = 0: zeroed at group begin
                     }
                 }
                 if (s_fresh[0] | s_fresh[1]) {   // lane refill: r^0 = 0 for a frame starting in this pass
@@ -492,9 +531,11 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
                         r2[s] = make_float2(ro[0][s], ro[1][s]);
                     }
                     uint2 d1 = make_uint2(0, 0);
-                    const uint2 c2 = cn_pair<RULE, NA, ND>(
+                    void* prv = MSG ? static_cast<void*>(reinterpret_cast<unsigned int*>(g.r) + size_t(ab) * 32 + lane)
+                                    : static_cast<void*>(pr);
+                    const uint2 c2 = cn_pair<RULE, NA, ND, MSG>(
                         tabk, L2, r2, make_float2(lam[0], lam[1]), make_uint2((swx >> lane) & 1u, (swy >> lane) & 1u),
-                        make_uint2((wv.x >> lane) & 1u, (wv.y >> lane) & 1u), pr, g.L, offs, d1);
+                        make_uint2((wv.x >> lane) & 1u, (wv.y >> lane) & 1u), prv, g.L, offs, d1);
                     chk[0] = c2.x;
                     chk[1] = c2.y;
                     b[0] = d1.x;
@@ -564,9 +605,10 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
 constexpr int kPipeStages = METLDPC_PIPE_STAGES;
 constexpr int kSmemPerSm = 232448;     // opt-in dynamic shared memory per block (227 KB)
 
-template <int NA, int ND>
+template <int NA, int ND, int MSG = 0>
 struct PipeCfg {
-    static constexpr int STG = (NA + ND) * 256;                       // bytes per stage: r, lambda
+    static constexpr int RB = MSG ? 128 : 256;                        // bytes per r row (64 lanes)
+    static constexpr int STG = NA * RB + ND * 256;                    // bytes per stage: r, lambda
     static constexpr int IDX = 32 * NA;                               // ints per staged tile
     static constexpr int WARP_BYTES = (2 * IDX * 4 + kPipeStages * STG + kPipeStages * 8 + 127) / 128 * 128;
     static constexpr int TAB = (PhiT<METLDPC_RULE_EXACT>::TAB_BYTES > PhiT<METLDPC_RULE_PHI_LUT>::TAB_BYTES)
@@ -609,11 +651,11 @@ __device__ __forceinline__ void tma_load_1d_ef(uint32_t dst, const void* src, ui
         : "memory");
 }
 
-template <int RULE, int NA, int ND>
-__global__ void __launch_bounds__(PipeCfg<NA, ND>::THREADS, 1)
+template <int RULE, int NA, int ND, int MSG = 0>
+__global__ void __launch_bounds__(PipeCfg<NA, ND, MSG>::THREADS, 1)
     k_cn_pipe(CodeDev cd, Group g, CnCtl karg, int begin, int count) {
     using PT = PhiT<RULE>;
-    using PC = PipeCfg<NA, ND>;
+    using PC = PipeCfg<NA, ND, MSG>;
     constexpr int TS = 32;                     // CNs per tile
     extern __shared__ __align__(16) char smem[];
     __shared__ uint32_t s_unsat[2], s_act[2], s_fresh[2];
@@ -663,8 +705,8 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND>::THREADS, 1)
             const uint32_t st = np % kPipeStages;
             const uint32_t bar = bar_a + 8 * st, dst = stage_a + st * PC::STG;
             mbar_expect_tx(bar, PC::STG);
-            tma_load_1d_ef(dst, g.r + size_t(abase + jl * NA) * 64, NA * 256, bar, pol);
-            if constexpr (ND > 0) tma_load_1d_ef(dst + NA * 256, g.lam1 + size_t(dbase + jl) * 64, 256, bar, pol);
+            tma_load_1d_ef(dst, reinterpret_cast<const char*>(g.r) + size_t(abase + jl * NA) * PC::RB, NA * PC::RB, bar, pol);
+            if constexpr (ND > 0) tma_load_1d_ef(dst + NA * PC::RB, g.lam1 + size_t(dbase + jl) * 64, 256, bar, pol);
         }
         ++np;
         if (++pi == min(TS, count - pt * TS)) { pi = 0; pt += GW; }
@@ -710,7 +752,8 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND>::THREADS, 1)
             const float* sr = reinterpret_cast<const float*>(stage + st * PC::STG);
 #pragma unroll
             for (int s = 0; s < NA; ++s) {
-                r2[s] = make_float2(sr[s * 64 + lane], sr[s * 64 + 32 + lane]);
+                if constexpr (MSG) r2[s] = msg16_q(reinterpret_cast<const uint32_t*>(sr)[s * 32 + lane]);   // q (N7)
+                else r2[s] = make_float2(sr[s * 64 + lane], sr[s * 64 + 32 + lane]);
             }
             // r^0 = 0 for a lane whose frame starts in this pass (Step 2), applied in registers:
             // the ring stages are written only by the TMA (async proxy), never by the threads
@@ -723,11 +766,12 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND>::THREADS, 1)
                 }
             }
             float2 lam = make_float2(0.0f, 0.0f);
-            if constexpr (ND > 0) lam = make_float2(sr[NA * 64 + lane], sr[NA * 64 + 32 + lane]);
-            float* pr = g.r + (size_t(abase + jl * NA) * 64 + lane);
+            if constexpr (ND > 0) lam = make_float2(sr[NA * PC::RB / 4 + lane], sr[NA * PC::RB / 4 + 32 + lane]);
+            void* pr = MSG ? static_cast<void*>(reinterpret_cast<unsigned int*>(g.r) + (size_t(abase + jl * NA) * 32 + lane))
+                           : static_cast<void*>(g.r + (size_t(abase + jl * NA) * 64 + lane));
             uint2 d1 = make_uint2(0, 0);
-            const uint2 c2 = cn_pair<RULE, NA, ND>(tabk, L2, r2, lam, make_uint2((swx >> lane) & 1u, (swy >> lane) & 1u),
-                                                   make_uint2((wv.x >> lane) & 1u, (wv.y >> lane) & 1u), pr, g.L, offs, d1);
+            const uint2 c2 = cn_pair<RULE, NA, ND, MSG>(tabk, L2, r2, lam, make_uint2((swx >> lane) & 1u, (swy >> lane) & 1u),
+                                                        make_uint2((wv.x >> lane) & 1u, (wv.y >> lane) & 1u), pr, g.L, offs, d1);
             un0 |= __ballot_sync(FULL, c2.x);
             un1 |= __ballot_sync(FULL, c2.y);
             if constexpr (ND > 0) {
@@ -797,8 +841,15 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group 
             if (s < na) {
                 const int v = __shfl_sync(FULL, idx, s);
                 const float Lv = __ldg(g.L + size_t(v) * 2 * g.B + off);
-                const float ro = ((g.fresh[c] >> lane) & 1u) ? 0.0f : __ldcs(g.r + size_t(ab + s) * g.B + off);
-                x = __fsub_rn(Lv, ro);
+                if (g.msg16) {   // 16-bit row (N7): half-word c of word `lane`; x = L - q 2^-10 (one rounding)
+                    const uint32_t w = ((g.fresh[c] >> lane) & 1u) ? 0x8080u
+                        : uint32_t(__ldcs(reinterpret_cast<const unsigned short*>(g.r) + size_t(ab + s) * 64 + 2 * lane + c));
+                    const float q = __fsub_rn(__uint_as_float(0x4B000000u | w), kMsg16Magic);
+                    x = __fmaf_rn(q, -0.0009765625f, Lv);
+                } else {
+                    const float ro = ((g.fresh[c] >> lane) & 1u) ? 0.0f : __ldcs(g.r + size_t(ab + s) * g.B + off);
+                    x = __fsub_rn(Lv, ro);
+                }
                 chk ^= uint32_t(Lv < 0.0f);
             } else {
                 const int q = db + (s - na);
@@ -839,7 +890,11 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group 
             {
                 const int v = __shfl_sync(FULL, idx, s);      // whole warp: lane s may be an idle lane
                 if (act) {
-                    __stcs(g.r + size_t(ab + s) * g.B + off, o);
+                    if (g.msg16)
+                        __stcs(reinterpret_cast<unsigned short*>(g.r) + size_t(ab + s) * 64 + 2 * lane + c,
+                               (unsigned short)(__float_as_uint(__fmaf_rn(o, 1024.0f, kMsg16Magic)) & 0xFFFFu));
+                    else
+                        __stcs(g.r + size_t(ab + s) * g.B + off, o);
                     atomicAdd(reinterpret_cast<unsigned int*>(g.L + size_t(v) * 2 * g.B + g.B + off), vn_fix(o));
                 }
             }
@@ -1531,43 +1586,52 @@ void launch_counters(int batch, const int32_t* iters, const uint8_t* conv, int64
 
 // ------------------------------------------------------------------ launchers
 
-template <int RULE, int NA, int ND>
-static void* cn_tile_fn() { return reinterpret_cast<void*>(&k_cn_tile<RULE, NA, ND>); }
+template <int RULE, int NA, int ND, int MSG>
+static void* cn_tile_fn() { return reinterpret_cast<void*>(&k_cn_tile<RULE, NA, ND, MSG>); }
 
-template <int RULE, int D = 0>
+template <int RULE, int MSG, int D = 0>
 static void* cn_tile_kernel(int d, int nd) {
     if constexpr (D <= kMaxUnrolledCnDeg) {
         if (d == D) {
-            if constexpr (D == 0) return cn_tile_fn<RULE, 0, 0>();
-            else return nd ? cn_tile_fn<RULE, D - 1, 1>() : cn_tile_fn<RULE, D, 0>();
+            if constexpr (D == 0) return cn_tile_fn<RULE, 0, 0, MSG>();
+            else return nd ? cn_tile_fn<RULE, D - 1, 1, MSG>() : cn_tile_fn<RULE, D, 0, MSG>();
         }
-        return cn_tile_kernel<RULE, D + 1>(d, nd);
+        return cn_tile_kernel<RULE, MSG, D + 1>(d, nd);
     } else {
         return nullptr;
     }
 }
 
-static void* cn_kernel(int rule, int D, int nd) {
+static void* cn_kernel(int rule, int D, int nd, int msg16) {
     if (D < 0)
         return rule == METLDPC_RULE_EXACT ? reinterpret_cast<void*>(&k_cn_generic<METLDPC_RULE_EXACT>)
                                           : reinterpret_cast<void*>(&k_cn_generic<METLDPC_RULE_PHI_LUT>);
-    return rule == METLDPC_RULE_EXACT ? cn_tile_kernel<METLDPC_RULE_EXACT>(D, nd)
-                                      : cn_tile_kernel<METLDPC_RULE_PHI_LUT>(D, nd);
+    if (msg16)
+        return rule == METLDPC_RULE_EXACT ? cn_tile_kernel<METLDPC_RULE_EXACT, 1>(D, nd)
+                                          : cn_tile_kernel<METLDPC_RULE_PHI_LUT, 1>(D, nd);
+    return rule == METLDPC_RULE_EXACT ? cn_tile_kernel<METLDPC_RULE_EXACT, 0>(D, nd)
+                                      : cn_tile_kernel<METLDPC_RULE_PHI_LUT, 0>(D, nd);
 }
 
-template <int RULE>
-static void* cn_pipe_kernel(int na, int nd) {
+template <int RULE, int MSG>
+static void* cn_pipe_kernel_m(int na, int nd) {
     switch (na * 2 + nd) {
-        case 2: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 1, 0>);
-        case 3: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 1, 1>);
-        case 4: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 2, 0>);
-        case 5: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 2, 1>);
-        case 6: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 3, 0>);
-        case 7: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 3, 1>);
-        case 8: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 4, 0>);
-        case 9: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 4, 1>);
+        case 2: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 1, 0, MSG>);
+        case 3: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 1, 1, MSG>);
+        case 4: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 2, 0, MSG>);
+        case 5: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 2, 1, MSG>);
+        case 6: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 3, 0, MSG>);
+        case 7: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 3, 1, MSG>);
+        case 8: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 4, 0, MSG>);
+        case 9: return reinterpret_cast<void*>(&k_cn_pipe<RULE, 4, 1, MSG>);
     }
     return nullptr;
+}
+
+static void* cn_pipe_kernel(int rule, int na, int nd, int msg16) {
+    if (rule == METLDPC_RULE_EXACT)
+        return msg16 ? cn_pipe_kernel_m<METLDPC_RULE_EXACT, 1>(na, nd) : cn_pipe_kernel_m<METLDPC_RULE_EXACT, 0>(na, nd);
+    return msg16 ? cn_pipe_kernel_m<METLDPC_RULE_PHI_LUT, 1>(na, nd) : cn_pipe_kernel_m<METLDPC_RULE_PHI_LUT, 0>(na, nd);
 }
 
 // Pipelined kernel for classes with 1..4 active slots and <= 1 degree-1 slot (64-lane
@@ -1580,27 +1644,33 @@ bool cn_use_pipe(int D, int nd) {
     return on && D >= 0 && nd <= 1 && D - nd >= 1 && D - nd <= 4;
 }
 
-template <int NA, int ND>
+template <int NA, int ND, int MSG>
 static void pipe_geom(int rule, int* threads, size_t* smem) {
-    using PC = PipeCfg<NA, ND>;
+    using PC = PipeCfg<NA, ND, MSG>;
     *threads = PC::THREADS;
     *smem = size_t(rule == METLDPC_RULE_EXACT ? PhiT<METLDPC_RULE_EXACT>::TAB_BYTES : PhiT<METLDPC_RULE_PHI_LUT>::TAB_BYTES) +
             size_t(PC::WARPS) * PC::WARP_BYTES;
 }
 
-static void cn_pipe_geom(int rule, int D, int nd, int* threads, size_t* smem) {
+template <int MSG>
+static void cn_pipe_geom_m(int rule, int D, int nd, int* threads, size_t* smem) {
     switch ((D - nd) * 2 + nd) {
-        case 2: pipe_geom<1, 0>(rule, threads, smem); return;
-        case 3: pipe_geom<1, 1>(rule, threads, smem); return;
-        case 4: pipe_geom<2, 0>(rule, threads, smem); return;
-        case 5: pipe_geom<2, 1>(rule, threads, smem); return;
-        case 6: pipe_geom<3, 0>(rule, threads, smem); return;
-        case 7: pipe_geom<3, 1>(rule, threads, smem); return;
-        case 8: pipe_geom<4, 0>(rule, threads, smem); return;
-        case 9: pipe_geom<4, 1>(rule, threads, smem); return;
+        case 2: pipe_geom<1, 0, MSG>(rule, threads, smem); return;
+        case 3: pipe_geom<1, 1, MSG>(rule, threads, smem); return;
+        case 4: pipe_geom<2, 0, MSG>(rule, threads, smem); return;
+        case 5: pipe_geom<2, 1, MSG>(rule, threads, smem); return;
+        case 6: pipe_geom<3, 0, MSG>(rule, threads, smem); return;
+        case 7: pipe_geom<3, 1, MSG>(rule, threads, smem); return;
+        case 8: pipe_geom<4, 0, MSG>(rule, threads, smem); return;
+        case 9: pipe_geom<4, 1, MSG>(rule, threads, smem); return;
     }
     *threads = 0;
     *smem = 0;
+}
+
+static void cn_pipe_geom(int rule, int D, int nd, int msg16, int* threads, size_t* smem) {
+    if (msg16) cn_pipe_geom_m<1>(rule, D, nd, threads, smem);
+    else cn_pipe_geom_m<0>(rule, D, nd, threads, smem);
 }
 
 int cn_tile_max(int D, int nd) { return (D - nd) <= 4 ? 32 : 8; }
@@ -1614,18 +1684,17 @@ size_t cn_smem(int rule, int D, int nd) {
     return tab + size_t(kCnThreads / 32) * cn_tile_max(D, nd) * na * sizeof(int);
 }
 
-int cn_blocks_per_sm(int rule, int D, int nd) {
+int cn_blocks_per_sm(int rule, int D, int nd, int msg16) {
     if (cn_use_pipe(D, nd)) {
-        void* f = rule == METLDPC_RULE_EXACT ? cn_pipe_kernel<METLDPC_RULE_EXACT>(D - nd, nd)
-                                             : cn_pipe_kernel<METLDPC_RULE_PHI_LUT>(D - nd, nd);
+        void* f = cn_pipe_kernel(rule, D - nd, nd, msg16);
         int th;
         size_t sm;
-        cn_pipe_geom(rule, D, nd, &th, &sm);
+        cn_pipe_geom(rule, D, nd, msg16, &th, &sm);
         cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         return 1;
     }
     int nb = 0;
-    void* f = cn_kernel(rule, D, nd);
+    void* f = cn_kernel(rule, D, nd, msg16);
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cn_smem(rule, D, nd)));
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kCnThreads, cn_smem(rule, D, nd)) != cudaSuccess) nb = 1;
     return nb > 0 ? nb : 1;
@@ -1740,16 +1809,15 @@ void launch_cn(const CodeDev& cd, const Group& g, int rule, int D, int nd, int b
                int l, bool check, cudaStream_t s, const L2Window& w, bool pdl) {
     CnCtl k{check ? 1 : 0, (l - 1) & 1, l & 1, l == 0 ? 1 : 0, check ? 1 : 0};
     if (cn_use_pipe(D, nd)) {
-        void* f = rule == METLDPC_RULE_EXACT ? cn_pipe_kernel<METLDPC_RULE_EXACT>(D - nd, nd)
-                                             : cn_pipe_kernel<METLDPC_RULE_PHI_LUT>(D - nd, nd);
+        void* f = cn_pipe_kernel(rule, D - nd, nd, g.msg16);
         int th;
         size_t sm;   // the smem attribute was set by cn_blocks_per_sm
-        cn_pipe_geom(rule, D, nd, &th, &sm);
+        cn_pipe_geom(rule, D, nd, g.msg16, &th, &sm);
         void* args[] = {const_cast<CodeDev*>(&cd), const_cast<Group*>(&g), &k, &begin, &count};
         launch_with_window(f, dim3(grid), dim3(th), args, sm, s, w, pdl);
         return;
     }
-    void* f = cn_kernel(rule, D, nd);
+    void* f = cn_kernel(rule, D, nd, g.msg16);
     if (D < 0) {
         void* args[] = {const_cast<CodeDev*>(&cd), const_cast<Group*>(&g), &k, &begin, &count};
         launch_with_window(f, dim3(grid), dim3(kCnThreads), args, cn_smem(rule, D, nd), s, w, pdl);

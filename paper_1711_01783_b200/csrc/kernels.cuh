@@ -13,7 +13,9 @@ namespace metldpc {
 // consecutive").  C = B / 32 lane chunks; bit vectors over lanes are uint32 per chunk.
 struct Group {
     int B, C;
-    float* r;          // [E_it][B]   CN->VN messages r_ji of active edges (Eqs. 2-3)
+    int msg16;         // 1: r rows hold 16-bit messages (N7; 64-lane groups only)
+    float* r;          // [E_it][B]   CN->VN messages r_ji of active edges (Eqs. 2-3); with msg16
+                       //             [E_it][32] uint32 words, word t = lanes t (low), t + 32 (high)
     float* L;          // [n_a][2][B] row of VN a: posterior LLR L (Eq. 5) at +0, the fixed-point
                        //             accumulator of the next L (uint32, N3) at +B
     float* lam_a;      // [n_a][B]    channel LLR of active VNs (Eq. 1)
@@ -80,11 +82,11 @@ struct L2Window {          // persisting-L2 access window (bytes == 0: none)
 
 // CN class kernels: total degree D in 0..16 with nd <= 1 degree-1 slots (tiled, unrolled)
 // or D = -1 (generic: more degree-1 slots or degree 17..32)
-int cn_blocks_per_sm(int rule, int D, int nd);
+int cn_blocks_per_sm(int rule, int D, int nd, int msg16);
 int cn_tile_max(int D, int nd);          // CNs per warp tile the kernel stages
 int cn_units_per_tile(int D, int nd);    // warp units per tile (1: both chunks, 2: one each)
 extern const int kCnThreadsHost;
-size_t cn_smem(int rule, int D);
+size_t cn_smem(int rule, int D, int nd);
 int finish_blocks_per_sm();
 
 void launch_scatter(const CodeDev& cd, const Group& g, const float* llr, int nb, cudaStream_t s);

@@ -27,21 +27,23 @@ def throughput_from_latency(n: int, iters: int, latency_s: float) -> float:
     return n / (iters * latency_s)
 
 
-def bytes_per_cw_iter(E_it: int, n_1: int, n_a: int, m: int, s: int = 4) -> dict:
-    """Byte model per codeword-iteration (fp32 messages, s = 4 bytes).
+def bytes_per_cw_iter(E_it: int, n_1: int, n_a: int, m: int, s: int = 4, s_r: int | None = None) -> dict:
+    """Byte model per codeword-iteration (fp32 node arrays, s = 4 bytes; edge messages of
+    s_r bytes, 4 = fp32 or 2 = the 16-bit storage of DESIGN.md N7).
 
     alg      : the method's floor -- each iterating edge message read once and
                written once, each degree-1 prior read once, each active VN
                prior read once and posterior written once and read once, plus
-               the syndrome bits: s(2 E_it + n_1 + 3 n_a) + m/8.
-    cn       : this build's check-node pass -- r read + r written (2 E_it s),
+               the syndrome bits: 2 E_it s_r + s(n_1 + 3 n_a) + m/8.
+    cn       : this build's check-node pass -- r read + r written (2 E_it s_r),
                degree-1 priors (n_1 s), posterior L read once (n_a s; the
                E_it gathers are L2 hits by design), syndrome bits (m/8).
-    vn       : this build's variable-node pass -- r read again (E_it s),
+    vn       : this build's variable-node pass -- r read again (E_it s_r),
                prior and posterior of every active VN (2 n_a s).
     two_pass : cn + vn.
     """
-    alg = s * (2 * E_it + n_1 + 3 * n_a) + m / 8.0
-    cn = s * (2 * E_it + n_1 + n_a) + m / 8.0
-    vn = s * (E_it + 2 * n_a)
+    s_r = s if s_r is None else s_r
+    alg = 2 * E_it * s_r + s * (n_1 + 3 * n_a) + m / 8.0
+    cn = 2 * E_it * s_r + s * (n_1 + n_a) + m / 8.0
+    vn = E_it * s_r + s * 2 * n_a
     return {"alg": alg, "cn": cn, "vn": vn, "two_pass": cn + vn}
