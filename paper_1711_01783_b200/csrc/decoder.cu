@@ -177,6 +177,14 @@ metldpc_status upload(T** dst, const std::vector<T>& src) {
     return METLDPC_OK;
 }
 
+// 16 bytes of zero padding after an index array: the CN ring kernel copies word ranges rounded
+// up to 16 bytes (kernels.cu ring_copy_words)
+std::vector<int32_t> padded(const std::vector<int32_t>& v) {
+    std::vector<int32_t> p(v);
+    p.resize(v.size() + 8, 0);
+    return p;
+}
+
 metldpc_status check_device(int32_t device, int* num_sms) {
     int count = 0;
     cudaError_t e = cudaGetDeviceCount(&count);
@@ -598,7 +606,7 @@ metldpc_status metldpc_code_create_ex(int32_t device, int32_t n, int32_t m, int6
     const HostLayout& L = c->host;
     const std::vector<float> te = phi_device_table(METLDPC_RULE_EXACT), tl = phi_device_table(METLDPC_RULE_PHI_LUT);
     if ((s = upload(&c->d_cn_aptr, L.cn_aptr)) || (s = upload(&c->d_cn_dptr, L.cn_dptr)) ||
-        (s = upload(&c->d_a_vn, L.a_vn)) || (s = upload(&c->d_vn_aptr, L.vn_aptr)) ||
+        (s = upload(&c->d_a_vn, padded(L.a_vn))) || (s = upload(&c->d_vn_aptr, L.vn_aptr)) ||
         (s = upload(&c->d_vn_aedge, L.vn_aedge)) || (s = upload(&c->d_vmap, L.vmap)) ||
         (s = upload(&c->d_cn_new, L.cn_new)) || (s = upload(&c->d_csr_ptr, L.csr_ptr)) ||
         (s = upload(&c->d_csr_vn, L.csr_vn)) ||
@@ -693,7 +701,7 @@ metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, cons
     for (auto& w : d->ws) {
         if ((s = dalloc(&w.r, size_t(L.E_it) * B * size_t(cfg.msg_bits) / 32)) || (s = dalloc(&w.L, 2 * size_t(L.n_a) * B)) ||
             (s = dalloc(&w.lam_a, size_t(L.n_a) * B)) || (s = dalloc(&w.lam1, size_t(L.n_1) * B)) ||
-            (s = dalloc(&w.d1bits, 2 * size_t(L.n_1) * C)) || (s = dalloc(&w.synd_t, size_t(L.m) * C)) ||
+            (s = dalloc(&w.d1bits, 2 * size_t(L.n_1) * C + 8)) || (s = dalloc(&w.synd_t, size_t(L.m) * C + 8)) ||
             (s = dalloc(&w.ctl, 32)) || (s = dalloc(&w.iters, B)) || (s = dalloc(&w.conv, B)) ||
             (s = dalloc(&w.lane_l, B)) || (s = dalloc(&w.lane_frame, B)) || (s = dalloc(&w.lane_fbuf, B)) ||
             (s = dalloc(&w.done, 1))) {
