@@ -44,10 +44,14 @@ PAPER_MBPS = 30.39           # PAPER.md Table 1 (lines 69-72), rate 0.1, TITAN X
 PAPER_TABLE1_MBPS = {"r0.1": (30.39, 27.54), "r0.05": (21.23, 18.49), "r0.02": (16.41, 14.00)}
 
 
+# stand-in family -> the Table-1 column (code rate) it reproduces the counts of
+RATE_COLUMN = {"r0.1": "r0.1", "r0.1de": "r0.1", "r0.05": "r0.05", "r0.02": "r0.02"}
+
+
 def paper_mbps(a) -> float | None:
-    if a.n != 1_000_000 or a.family not in PAPER_TABLE1_MBPS:
+    if a.n != 1_000_000 or a.family not in RATE_COLUMN:
         return None
-    return PAPER_TABLE1_MBPS[a.family][1 if a.no_skip else 0]
+    return PAPER_TABLE1_MBPS[RATE_COLUMN[a.family]][1 if a.no_skip else 0]
 SUSTAINED_NOTE = "HBM peak = MEASURED_PEAKS.json hbm_gbs (STREAM-style copy, measured)"
 
 
@@ -186,7 +190,7 @@ def measured_peak_gbs() -> tuple[float, str]:
 
 
 def workload_name(a) -> str:
-    tag = {"r0.1": "C3", "r0.05": "C4", "r0.02": "C6"}.get(a.family, "custom") if a.n == 1_000_000 else "custom"
+    tag = {"r0.1": "C3", "r0.1de": "C3", "r0.05": "C4", "r0.02": "C6"}.get(a.family, "custom") if a.n == 1_000_000 else "custom"
     return (f"{tag}: MET-LDPC {a.family} stand-in n={a.n}, SNR {a.snr}, max {a.iters} iterations "
             f"{'fixed' if a.no_et else 'with per-frame syndrome early termination'}, "
             f"{a.frames} frames/GPU per step, 8-D MD LLR input"
@@ -510,7 +514,7 @@ def main():
                        "parallelism": f"dp{world} (frames sharded f mod G; per-step NCCL all-reduce of the FER "
                                       "counters, one all-gather of per-frame results)"},
             "baseline_context": (f"vs_baseline = value / {paper_mbps(a)} Mb/s: paper Table 1 rate "
-                                 f"{a.family[1:]} {'without' if a.no_skip else 'with'} skipping on one TITAN Xp "
+                                 f"{RATE_COLUMN[a.family][1:]} {'without' if a.no_skip else 'with'} skipping on one TITAN Xp "
                                  "(64 codewords, fixed N iterations) -- context, other hardware")
                                 if paper_mbps(a) else None,
             "info_mbps": value * R, "goodput_info_mbps": value * R * conv_frac,

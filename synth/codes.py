@@ -12,6 +12,10 @@ structural count of Table 1 exactly at n = 10^6:
 * ``r0.05``: nu = 0.04 x1^2 x2^34 + 0.03 x1^3 x2^34 + 0.93 x3,
   mu = 0.01 x1^8 + 0.01 x1^9 + 0.41 x2^2 x3 + 0.52 x2^3 x3.
   n=10^6: E = 3,480,000, m = 950,000, 930,000 degree-1 VNs, E_it = 2,550,000.
+* ``r0.1de`` (R29): the same Table-1 counts with degrees chosen by density
+  evolution (tools/met_de.py): nu = 0.06375 x1^2 x2^21 + 0.0175 x1^3 x2^21 + 0.04375 x1^3 x2^20
+  + 0.875 x3, mu = 0.01375 x1^12 + 0.01125 x1^13 + 0.04375 x2^2 x3 + 0.83125 x2^3 x3
+  (DE threshold SNR 0.152 vs 0.182 for ``r0.1``).
 * ``r0.02`` (R25): nu = 0.02 x1^2 x2^{56|57} + 0.02 x1^3 x2^{56|57} + 0.96 x3,
   mu = 0.02 x1^5 + 0.6025 x2^2 x3 + 0.3575 x2^3 x3 (inner degree 57 on 37,500 of the 40,000
   active VNs).  n=10^6: E = 3,337,500, m = 980,000, 960,000 degree-1 VNs, E_it = 2,377,500.
@@ -118,6 +122,29 @@ def met_counts(family: str, n: int) -> dict:
         inner = {3: n1}                      # CNs x2^3 x3
         vn_core = {2: a2, 3: a3}
         inner_per_vn = 21
+    elif family == "r0.1de":
+        # DESIGN.md R29 / SURVEY 8(f) #4: same Table-1 counts (n_1 = 7n/8, m = n - 0.1 n,
+        # E_it = 2.8925 n, one degree-1 VN per inner check), degrees chosen by density evolution
+        # (tools/met_de.py): 5 % of the inner checks x2^2 x3, the rest x2^3 x3; the remaining
+        # iterating edges go to the core (VN core degrees 2/3, check degrees 12/13); inner VN
+        # degrees 20/21.  DE threshold SNR 0.152 (the r0.1 stand-in: 0.182).
+        if n % 8:
+            raise ValueError("r0.1de stand-in needs n divisible by 8")
+        a = n // 8
+        n1 = 7 * n // 8
+        m = n - int(round(0.1 * n))
+        t2 = int(round(0.05 * n1))
+        inner = {2: t2, 3: n1 - t2}
+        e2 = 2 * t2 + 3 * (n1 - t2)
+        e1 = int(round(2.8925 * n)) - e2
+        a3 = e1 - 2 * a
+        if not 0 <= a3 <= a:
+            raise ValueError("r0.1de stand-in infeasible at this n")
+        a2 = a - a3
+        vn_core = {2: a2, 3: a3}
+        lo, n_hi = divmod(e2, a)
+        # the inner degree lo + 1 goes to the first n_hi active VNs, i.e. core degree 2 first
+        inner_per_vn = np.concatenate([np.full(n_hi, lo + 1), np.full(a - n_hi, lo)])
     elif family == "r0.05":
         a = int(round(0.07 * n))
         a3 = int(round(3 * a / 7))

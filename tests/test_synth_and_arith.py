@@ -35,7 +35,7 @@ def test_structural_arithmetic_table1(col):
     assert col["total_edges"] - col["ignored_vns"] == col["iter_edges"]
 
 
-@pytest.mark.parametrize("family,idx", [("r0.1", 0), ("r0.05", 1), ("r0.02", 2)])
+@pytest.mark.parametrize("family,idx", [("r0.1", 0), ("r0.1de", 0), ("r0.05", 1), ("r0.02", 2)])
 def test_standin_codes_match_table1(family, idx):
     """The stand-in ensembles reproduce every structural count of Table 1 at n = 10^6."""
     col = T1["columns"][idx]
@@ -59,6 +59,30 @@ def test_standin_small_sizes():
         st = make_met_code("r0.1", n).stats()
         assert (st["m"], st["edges"], st["iter_edges"]) == (m, E, E_it)
     assert met_counts("r0.1", 10 ** 6)["core_deg"] == {10: 7500, 11: 17500}
+
+
+def test_r01de_degree_structure():
+    """DESIGN.md R29: the density-evolution stand-in at n = 10^6 has exactly the degree
+    distribution its DE threshold was computed for (tools/met_de.py R01DE)."""
+    c = make_met_code("r0.1de", 10 ** 6)
+    vd, cd = c.vn_degree, c.cn_degree
+    got = dict(zip(*[x.tolist() for x in np.unique(vd, return_counts=True)]))
+    # active VNs: (core 2, inner 21) 63,750 -> 23; (3, 21) 17,500 -> 24; (3, 20) 43,750 -> 23
+    assert got == {1: 875000, 23: 63750 + 43750, 24: 17500}
+    got = dict(zip(*[x.tolist() for x in np.unique(cd, return_counts=True)]))
+    assert got == {3: 43750, 4: 831250, 12: 13750, 13: 11250}
+
+
+def test_density_evolution_thresholds():
+    """SURVEY 8(f) #4 / DESIGN.md R29: discretised DE (tools/met_de.py) converges at the
+    headline SNR 0.161 for the r0.1de ensemble and not for the Table-1-count stand-in r0.1
+    (DE threshold 0.182, matching its measured waterfall, profiles/r1_c5_fer_sweep.jsonl)."""
+    import sys
+    sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1] / "tools"))
+    import met_de
+    ok_de, _, _ = met_de.de(met_de.R01DE, 0.161, iters=400)
+    ok_r01, _, _ = met_de.de(met_de.R01_STANDIN, 0.161, iters=400)
+    assert ok_de and not ok_r01
 
 
 def test_code_generation_deterministic(tmp_path, monkeypatch):

@@ -114,7 +114,7 @@ def de(ens: dict, s: float, iters: int = 400, tol: float = 1e-7, verbose: bool =
     core = ens["core"]        # list of (fraction of n, c)
     inner = ens["inner"]      # list of (fraction of n, e inner degree)  (each with one x3 socket)
     m1, m2 = ch.copy(), ch.copy()
-    pe_prev = 1.0
+    hist = []
     for it in range(1, iters + 1):
         # CN -> VN, type 1: core check of degree c, edge-perspective weight c k_c
         u1 = mix([(f * c, cpow(m1, c - 1)) for f, c in core])
@@ -142,13 +142,13 @@ def de(ens: dict, s: float, iters: int = 400, tol: float = 1e-7, verbose: bool =
             print(f"  it {it:4d}  Pe(active) {pe_active:.3e}  Pe(deg1) {pe1:.3e}", flush=True)
         if pe < tol:
             return True, it, (pe_active, pe1)
-        if it > 60 and pe > 0.999 * pe_prev and it % 20 == 0:
-            pass
-        pe_prev = pe
+        hist.append(pe)
+        if it > 40 and pe > 0.9999 * hist[-30]:   # no progress over 30 iterations: a fixed point
+            return False, it, (pe_active, pe1)
     return False, iters, (pe_active, pe1)
 
 
-def threshold(ens: dict, lo: float = 0.12, hi: float = 0.30, steps: int = 10, iters: int = 400) -> float:
+def threshold(ens: dict, lo: float = 0.14, hi: float = 0.22, steps: int = 8, iters: int = 600) -> float:
     for _ in range(steps):
         mid = 0.5 * (lo + hi)
         ok, it, pe = de(ens, mid, iters)
@@ -163,6 +163,35 @@ R01_STANDIN = {
     "act": [(0.1075, 2, 21), (0.0175, 3, 21)],
     "core": [(0.0075, 10), (0.0175, 11)],
     "inner": [(0.875, 3)],
+}
+
+def make_ensemble(act, core, inner):
+    """Checks the edge balance of a candidate: type 1 (sum a d = sum k c), type 2
+    (sum a b = sum t e), one degree-1 VN per inner check."""
+    e1v = sum(f * d for f, d, _ in act)
+    e1c = sum(f * c for f, c in core)
+    e2v = sum(f * b for f, _, b in act)
+    e2c = sum(f * e for f, e in inner)
+    assert abs(e1v - e1c) < 1e-9 and abs(e2v - e2c) < 1e-9, (e1v, e1c, e2v, e2c)
+    return {"act": act, "core": core, "inner": inner}
+
+
+def _thr(args):
+    name, ens = args
+    return name, threshold(ens)
+
+
+def run_many(cands: dict, procs: int = 8) -> dict:
+    from multiprocessing import Pool
+    with Pool(procs) as p:
+        return dict(p.map(_thr, list(cands.items())))
+
+
+# DESIGN.md R29 (synth/codes.py "r0.1de"): 5 % of the inner checks x2^2 x3; threshold 0.152
+R01DE = {
+    "act": [(0.06375, 2, 21), (0.0175, 3, 21), (0.04375, 3, 20)],
+    "core": [(0.01375, 12), (0.01125, 13)],
+    "inner": [(0.04375, 2), (0.83125, 3)],
 }
 
 if __name__ == "__main__":
