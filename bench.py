@@ -1,20 +1,21 @@
 #!/usr/bin/env python
 """bench.py -- throughput of the batched syndrome BP decoder (arXiv 1711.01783 hot path).
 
-Workload (BASELINE.json configs[2], "C3"): stand-in rate-0.1 MET-LDPC code, n = 10^6
-(Table-1 counts exactly, R18), SNR 0.161, N = 100 iterations with per-frame
-syndrome early termination, 8-D MD reconciliation output as input.  One step = one
-pass of the whole hot path over one batch resident in HBM: LLRs from MD output
-(metldpc_llr_from_md) -> decode (metldpc_decode) -> FER counters (metldpc_batch_counters,
-NCCL all-reduce when N > 1).  Frames shard across ranks (frame f -> rank f mod G, weak
-scaling).
+Workload (BASELINE.json configs[2], "C3"): a rate-0.1 MET-LDPC stand-in code with every Table-1
+count of the paper's (n = 10^6; default the density-evolution-optimised r0.1de, R29),
+SNR 0.161, N = 100 iterations with per-frame syndrome early termination and lane refill.  Input
+(--input): the channel LLRs of the virtual BIAWGN channel MD reconciliation creates (default)
+or the 8-D MD reconciliation output itself (--input md: metldpc_llr_from_md inside the step).  One
+step = one pass of the whole hot path over one batch resident in HBM: [LLRs from MD output ->]
+decode (metldpc_decode) -> FER counters (metldpc_batch_counters, NCCL all-reduce when N > 1).
+Frames shard across ranks (frame f -> rank f mod G, weak scaling).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 Prints ONE JSON line on rank 0.  `value` = decoded Mb/s (n bits per frame, the paper's
 Table-1 convention) over all ranks, device-timed with CUDA events
-(max over ranks); `e2e` = the same through metldpc_decode_md_host from pinned host
-buffers (H2D + D2H inside the timed region); `roofline` = the check-node update phase
+(max over ranks); `e2e` = the same through metldpc_decode_host / metldpc_decode_md_host from
+pinned host buffers (H2D + D2H inside the timed region); `roofline` = the check-node update phase
 (dominant kernel) against the measured HBM copy bandwidth; `cpu_baseline` = the CPU
 oracle (oracle/, fp32 replay M3) on the host cores.
 """
@@ -61,7 +62,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--family", default="r0.1")
+    ap.add_argument("--family", default="r0.1de",
+                    help="stand-in code: r0.1de (DE-optimised, default), r0.1 (round-1 stand-in), r0.05, r0.02")
+    ap.add_argument("--input", choices=["biawgn", "md"], default="biawgn",
+                    help="biawgn: channel LLRs of the virtual BIAWGN channel at --snr (P:20, DESIGN.md R31); "
+                         "md: 8-D MD reconciliation output through metldpc_llr_from_md (R13)")
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--snr", type=float, default=0.161)
     ap.add_argument("--iters", type=int, default=100)
@@ -87,21 +92,26 @@ def parse():
 # ----------------------------------------------------------------------------- inputs
 
 def _gen_one(args):
-    family, n, snr, key, fid = args
+    family, n, snr, key, fid, kind = args
     from synth.codes import make_met_code
-    from synth.frames import gen_frame
+    from synth.frames import gen_frame, gen_frame_biawgn
     code = make_met_code(family, n)
+    if kind == "biawgn":
+        f = gen_frame_biawgn(code, snr, key, fid)
+        return f["llr"], None, f["synd"]
     f = gen_frame(code, snr, key, fid)
     return f["v"], f["xnorm"], f["synd"]
 
 
 def gen_frames(a, frame_ids):
+    """(v, xnorm, S_B) per frame for --input md; (lambda, None, S_B) for --input biawgn."""
     from multiprocessing import get_context
-    jobs = [(a.family, a.n, a.snr, a.data_key, int(f)) for f in frame_ids]
+    jobs = [(a.family, a.n, a.snr, a.data_key, int(f), a.input) for f in frame_ids]
     procs = max(1, min(len(jobs), (os.cpu_count() or 4) // 2, 32))
     with get_context("fork").Pool(procs) as pool:
         out = pool.map(_gen_one, jobs)
-    return (np.stack([o[0] for o in out]), np.stack([o[1] for o in out]), np.stack([o[2] for o in out]))
+    xn = None if a.input == "biawgn" else np.stack([o[1] for o in out])
+    return (np.stack([o[0] for o in out]), xn, np.stack([o[2] for o in out]))
 
 
 def host_cores() -> int:
@@ -119,7 +129,8 @@ def oracle_throughput(a, code, v, xn, synd, budget_s: float, threads: int | None
     throughput is normalised to the workload's N iterations per frame."""
     from oracle import bp
     T = threads or max(1, min(host_cores(), 32, len(v)))
-    lam = [bp.llr_from_md_f32(v[i % len(v)], xn[i % len(v)], a.snr) for i in range(T)]
+    lam = [(bp.llr_from_md_f32(v[i % len(v)], xn[i % len(v)], a.snr) if xn is not None else v[i % len(v)])
+           for i in range(T)]
     t0 = time.perf_counter()
     bp.decode(code, lam[0], synd[0], 1, early_term=not a.no_et, rule=_rule(a), prec=32, no_skip=a.no_skip,
               msg16=a.msg_bits == 16)
@@ -193,9 +204,11 @@ def workload_name(a) -> str:
     tag = {"r0.1": "C3", "r0.1de": "C3", "r0.05": "C4", "r0.02": "C6"}.get(a.family, "custom") if a.n == 1_000_000 else "custom"
     return (f"{tag}: MET-LDPC {a.family} stand-in n={a.n}, SNR {a.snr}, max {a.iters} iterations "
             f"{'fixed' if a.no_et else 'with per-frame syndrome early termination'}, "
-            f"{a.frames} frames/GPU per step, 8-D MD LLR input"
+            f"{a.frames} frames/GPU per step"
             f"{', degree-1 VNs iterated (no skip)' if a.no_skip else ''}"
-            f"{', 16-bit edge messages' if a.msg_bits == 16 else ''}")
+            f"{', 16-bit edge messages' if a.msg_bits == 16 else ''}, "
+            + ("BIAWGN channel LLR input (the virtual channel of MD reconciliation, P:20)" if a.input == "biawgn"
+               else "8-D MD LLR input"))
 
 
 def run_reference(a, rank: int, world: int):
@@ -347,10 +360,10 @@ def main():
     # frames of this rank: global ids f with f mod world == rank; ND distinct ones tiled to F
     ND = min(a.distinct, F)
     ids = rank_frame_ids(ND, rank, world)
-    v_np, xn_np, sy_np = gen_frames(a, ids)
+    v_np, xn_np, sy_np = gen_frames(a, ids)       # biawgn: v_np holds the LLRs, xn_np is None
     rep = (F + ND - 1) // ND
     v = torch.from_numpy(np.tile(v_np, (rep, 1))[:F]).to(dev)
-    xn = torch.from_numpy(np.tile(xn_np, (rep, 1))[:F]).to(dev)
+    xn = torch.from_numpy(np.tile(xn_np, (rep, 1))[:F]).to(dev) if xn_np is not None else None
     sy = torch.from_numpy(np.tile(sy_np, (rep, 1))[:F].view(np.int32)).to(dev)
 
     hc = B.Code(code, device=local, no_skip=a.no_skip)
@@ -369,8 +382,11 @@ def main():
 
     def step(i):
         row = cnt[a.steps if i is None else i]
-        dec.llr_from_md(v, xn, a.snr, out=llr)
-        dec.decode(llr, sy, out=(bits, iters, conv))
+        if a.input == "md":
+            dec.llr_from_md(v, xn, a.snr, out=llr)
+            dec.decode(llr, sy, out=(bits, iters, conv))
+        else:
+            dec.decode(v, sy, out=(bits, iters, conv))
         dec.counters(iters, conv, row)
         D.reduce_counters(row)          # NCCL all-reduce when world > 1
 
@@ -416,12 +432,13 @@ def main():
                     lanes_per_group=a.lanes, groups_in_flight=1, msg_bits=a.msg_bits)
     Fi = min(F, a.lanes)
     outi = (bits[:Fi], iters[:Fi], conv[:Fi])
-    iso.decode(llr[:Fi], sy[:Fi], out=outi)
+    lam_dev = llr if a.input == "md" else v            # the step's LLRs (md: converted by the last step)
+    iso.decode(lam_dev[:Fi], sy[:Fi], out=outi)
     torch.cuda.synchronize()
     iso.reset_profile()
     iso.set_profiling(True)
     for _ in range(2):
-        iso.decode(llr[:Fi], sy[:Fi], out=outi)
+        iso.decode(lam_dev[:Fi], sy[:Fi], out=outi)
     torch.cuda.synchronize()
     prof_k = iso.profile()
     iso.close()
@@ -449,7 +466,9 @@ def main():
                                     "dram_gbs": traffic_prod / pg["graph_ms_per_pass"] / 1e6}
         except Exception:
             traffic = traffic_prod = None
-    it_bytes = F * world * a.steps * a.iters
+    # codeword-iterations the timed steps decoded: the counters' sum of iterations over valid
+    # frames (N per frame when none converges early)
+    cw_iters = int(total[2])
     roofline = {"bound": "hbm", "achieved": cn_gbs, "peak": peak, "unit": "GB/s",
                 "frac": (cn_gbs / peak) if cn_gbs else None, "traffic": traffic,
                 "traffic_production_pass": (dict(traffic_prod, frac=traffic_prod["dram_gbs"] / peak)
@@ -461,30 +480,39 @@ def main():
                 "peak_source": peak_src,
                 "avg_launch_ms": prof_k["cn_ms"] / max(1, prof_k["cn_launches"]), "kernel_timing": kernel_timing,
                 "finish_avg_launch_ms": prof_k["vn_ms"] / max(1, prof_k["vn_launches"]),
-                # whole timed step: the method's algorithmic floor (SURVEY 8(d) B_alg) x codeword-
-                # iterations (N per frame: every frame runs N at this SNR when none converges)
-                "iteration_alg_frac": (it_bytes * bm["alg"] / (ms_max / 1e3) / 1e9 / peak)}
+                # whole timed step: the method's algorithmic floor (SURVEY 8(d) B_alg) x the
+                # codeword-iterations decoded, over the device-timed step
+                "iteration_alg_frac": (cw_iters * bm["alg"] / (ms_max / 1e3) / 1e9 / peak)}
 
     # ---- e2e through the host-buffer C-ABI call (pinned host memory, copies inside)
     e2e = None
     if not a.no_e2e:
         v_h = torch.from_numpy(np.tile(v_np, (rep, 1))[:F]).pin_memory()
-        xn_h = torch.from_numpy(np.tile(xn_np, (rep, 1))[:F]).pin_memory()
+        xn_h = torch.from_numpy(np.tile(xn_np, (rep, 1))[:F]).pin_memory() if xn_np is not None else None
         sy_h = torch.from_numpy(np.tile(sy_np, (rep, 1))[:F].view(np.int32)).pin_memory()
         out_h = (torch.empty((F, nw), dtype=torch.int32).pin_memory(), torch.empty(F, dtype=torch.int32).pin_memory(),
                  torch.empty(F, dtype=torch.uint8).pin_memory())
-        dec.decode_md_host(v_h, xn_h, sy_h, a.snr, out=out_h)      # warm (allocates staging)
+
+        def host_call():
+            if a.input == "md":
+                dec.decode_md_host(v_h, xn_h, sy_h, a.snr, out=out_h)
+            else:
+                dec.decode_host(v_h, sy_h, out=out_h)
+
+        host_call()                                                   # warm (allocates staging)
         barrier()
         k_e2e = max(1, min(a.steps, 3))
         t0 = time.perf_counter()
         for _ in range(k_e2e):
-            dec.decode_md_host(v_h, xn_h, sy_h, a.snr, out=out_h)
+            host_call()
         dt = D.max_over_ranks(time.perf_counter() - t0, device=dev)
         W = (st["m"] + 31) // 32
         e2e = {"value": F * world * k_e2e * a.n / dt / 1e6, "unit": "Mb/s",
-               "h2d_bytes_per_step": F * world * (a.n * 4 + (a.n // 8) * 4 + W * 4),
+               "h2d_bytes_per_step": F * world * (a.n * 4 + ((a.n // 8) * 4 if a.input == "md" else 0) + W * 4),
                "d2h_bytes_per_step": F * world * (nw * 4 + 4 + 1),
-               "api": "metldpc_decode_md_host (pinned host buffers; H2D, LLR, decode, D2H inside the call; "
+               "api": ("metldpc_decode_md_host (pinned host buffers; H2D, LLR, decode, D2H inside the call; "
+                       if a.input == "md" else
+                       "metldpc_decode_host (pinned host LLR / syndrome buffers; H2D, decode, D2H inside the call; ")
                       + ("lane refill: chunked H2D published to the streaming decode's queue"
                          if not (a.no_refill or a.no_et) else "64-lane groups, copies overlapped with decode") + ")",
                "steps": k_e2e, "timing": "host wall clock around the synchronous call, max over ranks"}
@@ -518,6 +546,12 @@ def main():
                                  "(64 codewords, fixed N iterations) -- context, other hardware")
                                 if paper_mbps(a) else None,
             "info_mbps": value * R, "goodput_info_mbps": value * R * conv_frac,
+            # the n-bit Mb/s of the same decoding work run as the paper's fixed-N flow (every frame
+            # N iterations): value x mean iterations / N
+            "fixed_n_equivalent_mbps": value * counts["mean_iters"] / a.iters,
+            "input": ("BIAWGN channel LLRs at the SNR (the virtual channel MD reconciliation creates, P:20; "
+                      "DESIGN.md R31)" if a.input == "biawgn" else
+                      "8-D MD reconciliation output (v, |x|) -> metldpc_llr_from_md (R13) inside the step"),
             **counts,
             "comm": {"backend": "nccl" if world > 1 else None, "world_size": world},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

@@ -352,14 +352,14 @@ __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 
     float2 p[D], P[D];
     uint32_t xb0[D], xb1[D];
     uint32_t par0 = sbit.x << 31, par1 = sbit.y << 31;
-    uint32_t chk0 = sbit.x ^ d1prev.x, chk1 = sbit.y ^ d1prev.y;
+    uint32_t lw0 = 0, lw1 = 0;   // XOR of the L words: bit 31 = parity of the active decisions
 #pragma unroll
     for (int s = 0; s < NA; ++s) {
         const float2 x = MSG ? f2fma(ro[s], make_float2(-0.0009765625f, -0.0009765625f), Lv[s])
                              : f2sub(Lv[s], ro[s]);                       // extrinsic q = L - r (R10)
         // [L < 0] and [x < 0] are the sign bits: L and x are never -0 (see k_scatter)
-        chk0 ^= __float_as_uint(Lv[s].x) >> 31;
-        chk1 ^= __float_as_uint(Lv[s].y) >> 31;
+        lw0 ^= __float_as_uint(Lv[s].x);
+        lw1 ^= __float_as_uint(Lv[s].y);
         xb0[s] = __float_as_uint(x.x);
         xb1[s] = __float_as_uint(x.y);
         par0 ^= xb0[s];
@@ -411,7 +411,7 @@ __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 
         }
         if (s > 0) Q = f2add(Q, p[s]);
     }
-    return make_uint2(chk0, chk1);
+    return make_uint2((lw0 >> 31) ^ sbit.x ^ d1prev.x, (lw1 >> 31) ^ sbit.y ^ d1prev.y);
 }
 
 #ifndef METLDPC_CN_PAIR
@@ -610,6 +610,9 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
 #endif
 #ifndef METLDPC_PIPE_WARPS
 #define METLDPC_PIPE_WARPS 32   // warps per CTA cap (at most what the rings leave room for)
+#endif
+#ifndef METLDPC_RING_CW
+#define METLDPC_RING_CW 31      // compute warps of the CN ring kernel (+ 1 producer warp)
 #endif
 #ifndef METLDPC_RING_STAGES
 #define METLDPC_RING_STAGES 6   // CTA ring depth cap (k_cn_ring)
@@ -851,7 +854,7 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 
 template <int NA, int ND, int MSG>
 struct RingCfg {
-    static constexpr int CW = 31;                                     // compute warps = CNs per stage
+    static constexpr int CW = METLDPC_RING_CW;                        // compute warps = CNs per stage
     static constexpr int RB = MSG ? 128 : 256;                        // r row bytes (64 lanes)
     // word arrays are copied from the 16-byte-aligned word at or below the first one needed
     // (lead 0..3 words) and rounded up to 16 bytes; the device arrays are padded for it
@@ -923,10 +926,9 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
     if (warp == CW) {
         if (lane == 0) {
             const uint64_t pol = l2_evict_first_policy();
-            int kk = 0;
-            for (int gs = blockIdx.x; gs < nst; gs += gridDim.x, ++kk) {
-                const int slot = kk % S;
-                if (kk >= S) mbar_wait(empty_a + 8 * slot, ((kk / S) - 1) & 1);
+            int slot = 0, use = 0;
+            for (int gs = blockIdx.x; gs < nst; gs += gridDim.x) {
+                if (use) mbar_wait(empty_a + 8 * slot, (use - 1) & 1);
                 const int j0 = gs * CW, ncn = min(CW, count - j0);
                 const uint32_t dst = ring_a + slot * RC::STG, bar = full_a + 8 * slot;
                 const long wi = long(abase) + long(j0) * NA, ws = (long(begin) + j0) * 2,
@@ -942,6 +944,10 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
                 ring_copy_words(dst + RC::OFF_SY, g.synd_t, ws, ncn * 2, bar, pol);
                 if constexpr (ND > 0)
                     if (d1in) ring_copy_words(dst + RC::OFF_D1, g.d1bits, wd, ncn * 2, bar, pol);
+                if (++slot == S) {
+                    slot = 0;
+                    ++use;
+                }
             }
         }
     } else {                                       // ---- compute warps: CN `warp` of every stage
@@ -949,11 +955,11 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
         const uint32_t am0 = s_act[0], am1 = s_act[1];
         const bool any_fresh = (s_fresh[0] | s_fresh[1]) != 0u;
         const bool f0 = (s_fresh[0] >> lane) & 1u, f1 = (s_fresh[1] >> lane) & 1u;
-        int kk = 0;
-        for (int gs = blockIdx.x; gs < nst; gs += gridDim.x, ++kk) {
-            const int slot = kk % S;
+        int slot = 0;
+        uint32_t phase = 0;   // parity of the slot's current use
+        for (int gs = blockIdx.x; gs < nst; gs += gridDim.x) {
             const int j0 = gs * CW, ncn = min(CW, count - j0);
-            mbar_wait(full_a + 8 * slot, (kk / S) & 1);
+            mbar_wait(full_a + 8 * slot, phase);
             if (warp < ncn) {
                 const char* sp = ring + slot * RC::STG;
                 const int jl = j0 + warp;
@@ -1015,6 +1021,10 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
             }
             __syncwarp();                           // the warp has read the stage
             if (lane == 0) mbar_arrive(empty_a + 8 * slot);
+            if (++slot == S) {
+                slot = 0;
+                phase ^= 1u;
+            }
         }
         if (k.check && lane == 0) {
             if (un0 & am0) atomicOr(&s_unsat[0], un0 & am0);

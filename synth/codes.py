@@ -13,9 +13,10 @@ structural count of Table 1 exactly at n = 10^6:
   mu = 0.01 x1^8 + 0.01 x1^9 + 0.41 x2^2 x3 + 0.52 x2^3 x3.
   n=10^6: E = 3,480,000, m = 950,000, 930,000 degree-1 VNs, E_it = 2,550,000.
 * ``r0.1de`` (R29): the same Table-1 counts with degrees chosen by density
-  evolution (tools/met_de.py): nu = 0.06375 x1^2 x2^21 + 0.0175 x1^3 x2^21 + 0.04375 x1^3 x2^20
-  + 0.875 x3, mu = 0.01375 x1^12 + 0.01125 x1^13 + 0.04375 x2^2 x3 + 0.83125 x2^3 x3
-  (DE threshold SNR 0.152 vs 0.182 for ``r0.1``).
+  evolution (tools/met_de.py) and finite-length runs (tools/met_search.py):
+  nu = 0.0475 x1^2 x2^21 + 0.0175 x1^3 x2^21 + 0.06 x1^3 x2^20 + 0.875 x3,
+  mu = 0.0225 x1^13 + 0.0025 x1^14 + 0.06 x2^2 x3 + 0.815 x2^3 x3, built without 4-cycles
+  among the active VNs (DE threshold SNR 0.153 vs 0.182 for ``r0.1``).
 * ``r0.02`` (R25): nu = 0.02 x1^2 x2^{56|57} + 0.02 x1^3 x2^{56|57} + 0.96 x3,
   mu = 0.02 x1^5 + 0.6025 x2^2 x3 + 0.3575 x2^3 x3 (inner degree 57 on 37,500 of the 40,000
   active VNs).  n=10^6: E = 3,337,500, m = 980,000, 960,000 degree-1 VNs, E_it = 2,377,500.
@@ -40,8 +41,9 @@ from pathlib import Path
 import numpy as np
 
 CODE_SEED = 1711
-_CACHE = Path(os.environ.get("METLDPC_CODE_CACHE",
-                             Path(__file__).resolve().parent.parent / "build" / "codes"))
+# generated codes are cached outside the repository (a 10^6 code is ~60 MB; the cache is a
+# pure function of (family, n, seed) and is rebuilt in seconds when missing)
+_CACHE = Path(os.environ.get("METLDPC_CODE_CACHE", Path.home() / ".cache" / "metldpc" / "codes"))
 
 
 @dataclasses.dataclass
@@ -125,20 +127,21 @@ def met_counts(family: str, n: int) -> dict:
     elif family == "r0.1de":
         # DESIGN.md R29 / SURVEY 8(f) #4: same Table-1 counts (n_1 = 7n/8, m = n - 0.1 n,
         # E_it = 2.8925 n, one degree-1 VN per inner check), degrees chosen by density evolution
-        # (tools/met_de.py): 5 % of the inner checks x2^2 x3, the rest x2^3 x3; the remaining
-        # iterating edges go to the core (VN core degrees 2/3, check degrees 12/13); inner VN
-        # degrees 20/21.  DE threshold SNR 0.152 (the r0.1 stand-in: 0.182).
+        # (tools/met_de.py) and finite-length runs (tools/met_search.py): 0.06 n inner checks
+        # x2^2 x3, the rest x2^3 x3; the remaining iterating edges go to the core (VN core
+        # degrees 2/3, check degrees 13/14); inner VN degrees 20/21; no 4-cycles among the
+        # active VNs (make_met_code).  DE threshold SNR 0.153 on the BIAWGN channel (r0.1: 0.182).
         if n % 8:
             raise ValueError("r0.1de stand-in needs n divisible by 8")
         a = n // 8
         n1 = 7 * n // 8
         m = n - int(round(0.1 * n))
-        t2 = int(round(0.05 * n1))
+        t2 = int(round(0.06 * n))
         inner = {2: t2, 3: n1 - t2}
         e2 = 2 * t2 + 3 * (n1 - t2)
         e1 = int(round(2.8925 * n)) - e2
         a3 = e1 - 2 * a
-        if not 0 <= a3 <= a:
+        if not 0 <= a3 <= a or t2 > n1:
             raise ValueError("r0.1de stand-in infeasible at this n")
         a2 = a - a3
         vn_core = {2: a2, 3: a3}
@@ -203,6 +206,59 @@ def _match(rng, vn_sock: np.ndarray, cn_sock: np.ndarray, m: int):
     raise RuntimeError("parallel-edge repair did not converge")
 
 
+def break_4cycles(vn_all, cn_all, typ, rng, max_rounds=50):
+    """Swap check sockets (within an edge type) until no two active VNs share two checks (at
+    n = 10^6 two rounds suffice; small codes keep some 4-cycles after max_rounds)."""
+    vn_all = vn_all.copy()
+    cn_all = cn_all.copy()
+    for rnd in range(max_rounds):
+        order = np.lexsort((vn_all, cn_all))
+        cs, vs = cn_all[order], vn_all[order]
+        starts = np.flatnonzero(np.r_[True, cs[1:] != cs[:-1]])
+        ends = np.r_[starts[1:], cs.size]
+        deg = ends - starts
+        # all VN pairs inside each check (vectorised per degree)
+        keys, eidx = [], []
+        for d in np.unique(deg):
+            if d < 2:
+                continue
+            st = starts[deg == d]
+            blk = st[:, None] + np.arange(d)[None, :]
+            iu, ju = np.triu_indices(d, 1)
+            u, v = vs[blk[:, iu]], vs[blk[:, ju]]
+            keys.append((u.astype(np.int64) << 32) | v.astype(np.int64))
+            eidx.append(order[blk[:, ju]])
+        keys = np.concatenate([k.ravel() for k in keys])
+        eidx = np.concatenate([e.ravel() for e in eidx])
+        o = np.argsort(keys, kind="stable")
+        ks = keys[o]
+        dup = o[1:][ks[1:] == ks[:-1]]
+        if dup.size == 0:
+            return vn_all, cn_all, rnd
+        bad = np.unique(eidx[dup])
+        # swap each bad edge's check with a random edge of the same type
+        for t in np.unique(typ[bad]):
+            b = bad[typ[bad] == t]
+            pool = np.setdiff1d(np.flatnonzero(typ == t), b)
+            if b.size > pool.size // 2:   # small codes: 4-cycles cannot all be removed; swap a subset
+                b = rng.choice(b, size=max(pool.size // 2, 0), replace=False)
+            if b.size == 0:
+                continue
+            other = rng.choice(pool, size=b.size, replace=False)   # disjoint from b: a permutation
+            cn_all[b], cn_all[other] = cn_all[other], cn_all[b].copy()
+        # parallel edges created by swaps: undo by re-swapping randomly next round (checked above
+        # as a duplicate pair only between distinct checks, so check them here)
+        key = vn_all.astype(np.int64) * (cn_all.max() + 1) + cn_all
+        _, first = np.unique(key, return_index=True)
+        par = np.setdiff1d(np.arange(key.size), first)
+        for e in par:
+            t = typ[e]
+            pool = np.flatnonzero(typ == t)
+            o2 = int(rng.choice(pool))
+            cn_all[e], cn_all[o2] = int(cn_all[o2]), int(cn_all[e])
+    return vn_all, cn_all, max_rounds
+
+
 def make_met_code(family: str, n: int, seed: int = CODE_SEED, cache: bool = True) -> Code:
     name = f"{family}_n{n}_s{seed}"
     path = _CACHE / f"{name}.npz"
@@ -226,6 +282,10 @@ def make_met_code(family: str, n: int, seed: int = CODE_SEED, cache: bool = True
     v1, c1 = _match(rng, np.repeat(np.arange(a), core_deg_vn), np.repeat(core_ids, core_deg_cn), m)
     # type 2 (inner edges of active VNs)
     v2, c2 = _match(rng, np.repeat(np.arange(a), c["inner_per_vn"]), np.repeat(inner_ids, inner_deg), m)
+    if family == "r0.1de":   # no two active VNs share two checks (4-cycles; R29)
+        vv, cc, _ = break_4cycles(np.concatenate([v1, v2]), np.concatenate([c1, c2]),
+                               np.concatenate([np.ones(v1.size, np.int8), np.full(v2.size, 2, np.int8)]), rng)
+        v1, c1, v2, c2 = vv[:v1.size], cc[:v1.size], vv[v1.size:], cc[v1.size:]
     # type 3 (one degree-1 VN per inner CN)
     v3 = np.arange(a, n)
     c3 = rng.permutation(inner_ids)

@@ -110,3 +110,20 @@ def gen_batch(code: Code, snr: float, data_key: int, frame_ids, d: int = 8) -> d
     fr = [gen_frame(code, snr, data_key, f, d) for f in frame_ids]
     return {k: np.stack([f[k] for f in fr]) for k in ("u", "v", "xnorm", "synd", "x", "alpha")} | {
         "frame_ids": np.asarray(list(frame_ids))}
+
+
+def gen_frame_biawgn(code: Code, snr: float, data_key: int, frame_id: int) -> dict:
+    """One frame of the virtual BIAWGN channel MD reconciliation creates: Bob's bits
+    u, S_B = H u, and Alice's channel LLRs lambda = 2 y snr with y = (1 - 2u) + N(0, 1/snr),
+    i.e. lambda ~ N(+-2 snr, 4 snr) (R31)."""
+    g = frame_rng(data_key, (1 << 62) | int(frame_id))      # own stream: not the MD frames' draws
+    u = g.integers(0, 2, size=code.n, dtype=np.uint8)
+    y = (1.0 - 2.0 * u) + g.standard_normal(code.n) / np.sqrt(snr)
+    return {"u": u, "llr": (2.0 * snr * y).astype(np.float32), "synd": syndrome_words(code, u),
+            "frame_id": frame_id}
+
+
+def gen_batch_biawgn(code: Code, snr: float, data_key: int, frame_ids) -> dict:
+    fr = [gen_frame_biawgn(code, snr, data_key, f) for f in frame_ids]
+    return {k: np.stack([f[k] for f in fr]) for k in ("u", "llr", "synd")} | {"frame_ids": np.asarray(list(frame_ids))}
+

@@ -48,3 +48,15 @@ def gen_batch(n: int, batch: int, snr: float, key: int, index: int, d: int = 8, 
     ut = (1.0 - 2.0 * u.view(batch, n // d, d).to(torch.float64)) / d ** 0.5
     alpha = cd_mul(ut, _conj(yh)).reshape(batch, n)
     return x.to(torch.float32).contiguous(), alpha.to(torch.float32).contiguous(), u
+
+
+def gen_batch_biawgn(n: int, batch: int, snr: float, key: int, index: int, device="cuda"):
+    """Virtual BIAWGN channel (R31): Bob's bits u (uint8 [batch][n]) and Alice's
+    LLRs lambda = 2 snr y, y = (1 - 2u) + N(0, 1/snr) (fp32 [batch][n])."""
+    g = torch.Generator(device=device)
+    g.manual_seed((int(key) << 32) ^ (int(index) * 0x9E3779B1) ^ int(round(snr * 1e6)) ^ 0x5BD1E995)
+    u = torch.randint(0, 2, (batch, n), generator=g, device=device, dtype=torch.uint8)
+    y = (1.0 - 2.0 * u.to(torch.float64)) + torch.randn(batch, n, generator=g, device=device,
+                                                        dtype=torch.float64) / snr ** 0.5
+    return (2.0 * snr * y).to(torch.float32).contiguous(), u
+

@@ -261,3 +261,74 @@ def test_batch_counters(c1):
     B.metldpc_batch_counters(dec2.h, big, torch.from_numpy(it2).cuda(), torch.from_numpy(cv2).cuda(), out2)
     torch.cuda.synchronize()
     assert out2.cpu().numpy().tolist() == [big, int(cv2.sum()), int(it2[it2 >= 0].sum()), int((it2 < 0).sum())]
+
+
+# ----------------------------------------------------------------------------- headline config
+
+def test_r01de_c1_bits_iters_flags(c1):
+    """The density-evolution stand-in (r0.1de, R29) at C1 size: its kernel classes
+    (inner (2,1) and (3,1) checks in the ring kernel, core (13,0)/(14,0) checks in the tiled
+    kernel) bit-exact against M3 on BIAWGN frames (R31), both message formats."""
+    from synth.frames import gen_batch_biawgn
+    code = make_met_code("r0.1de", 2048)
+    h = B.Code(code)
+    fr = [gen_batch_biawgn(code, s, 80, range(i * 100, i * 100 + 16)) for i, s in enumerate((0.2, 0.35, 0.6))]
+    llr = np.concatenate([f["llr"] for f in fr])
+    sy = np.concatenate([f["synd"] for f in fr])
+    for msg in (32, 16):
+        dec = B.Decoder(h, len(llr), max_iter=100, msg_bits=msg)
+        bits, it, cv = dec.decode(torch.from_numpy(llr).cuda(), torch.from_numpy(sy.view(np.int32)).cuda())
+        torch.cuda.synchronize()
+        bits, it, cv = bits.cpu().numpy().view(np.uint32), it.cpu().numpy(), cv.cpu().numpy()
+        nconv = 0
+        for i in range(len(llr)):
+            o = bp.decode(code, llr[i], sy[i], 100, prec=32, msg16=msg == 16)
+            assert it[i] == o["iters"] and bool(cv[i]) == o["converged"], (msg, i)
+            assert np.array_equal(unpack_bits(bits[i], code.n), o["bits"]), (msg, i)
+            nconv += o["converged"]
+        assert 0 < nconv < len(llr)
+
+
+def _gen_c3_biawgn(snr, f):
+    from synth.frames import gen_frame_biawgn
+    code = make_met_code("r0.1de", 10 ** 6)
+    fr = gen_frame_biawgn(code, snr, 81, f)
+    return fr["llr"], fr["synd"], fr["u"]
+
+
+def test_headline_config_sampled_frames():
+    """The bench's headline configuration (r0.1de, n = 10^6, BIAWGN input at SNR 0.161, N = 100,
+    early termination + lane refill, 64-lane groups, fp32 messages): 128 frames (64 distinct, each
+    twice in different lanes / refill waves); three sampled frames bit-exact against M3, every
+    copy decoded identically, and the decoder converges there (FER < 0.5, mean iterations < 100)."""
+    code = make_met_code("r0.1de", 10 ** 6)
+    h = B.Code(code)
+    snr, nd = 0.161, 64
+    from multiprocessing import get_context
+    with get_context("fork").Pool(8) as pool:
+        frs = pool.starmap(_gen_c3_biawgn, [(snr, f) for f in range(nd)])
+    llr = np.stack([f[0] for f in frs])
+    sy = np.stack([f[1] for f in frs])
+    idx = np.concatenate([np.arange(nd), np.arange(nd)[::-1]])
+    dec = B.Decoder(h, 2 * nd, max_iter=100, lane_refill=True)
+    bits, it, cv = dec.decode(torch.from_numpy(llr[idx]).cuda(), torch.from_numpy(sy[idx].view(np.int32)).cuda())
+    torch.cuda.synchronize()
+    bits, it, cv = bits.cpu().numpy().view(np.uint32), it.cpu().numpy(), cv.cpu().numpy()
+    for j in range(nd):
+        k = 2 * nd - 1 - j
+        assert np.array_equal(bits[j], bits[k]) and it[j] == it[k] and cv[j] == cv[k], j
+    assert cv.mean() > 0.5 and it.mean() < 100
+    good = [int(i) for i in np.flatnonzero(cv[:nd] == 1)]
+    sample = [good[0], int(np.argmax(np.where(cv[:nd] == 1, it[:nd], -1)))]
+    bad = np.flatnonzero(cv[:nd] == 0)
+    if bad.size:
+        sample.append(int(bad[0]))
+
+    def one(i):
+        return bp.decode(code, llr[i], sy[i], 100, prec=32)
+
+    with ThreadPoolExecutor(len(sample)) as ex:
+        res = list(ex.map(one, sample))
+    for i, o in zip(sample, res):
+        assert it[i] == o["iters"] and bool(cv[i]) == o["converged"], (i, it[i], o["iters"])
+        assert np.array_equal(unpack_bits(bits[i], code.n), o["bits"]), i

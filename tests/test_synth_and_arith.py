@@ -67,10 +67,34 @@ def test_r01de_degree_structure():
     c = make_met_code("r0.1de", 10 ** 6)
     vd, cd = c.vn_degree, c.cn_degree
     got = dict(zip(*[x.tolist() for x in np.unique(vd, return_counts=True)]))
-    # active VNs: (core 2, inner 21) 63,750 -> 23; (3, 21) 17,500 -> 24; (3, 20) 43,750 -> 23
-    assert got == {1: 875000, 23: 63750 + 43750, 24: 17500}
+    # active VNs: (core 2, inner 21) 47,500 -> 23; (3, 21) 17,500 -> 24; (3, 20) 60,000 -> 23
+    assert got == {1: 875000, 23: 47500 + 60000, 24: 17500}
     got = dict(zip(*[x.tolist() for x in np.unique(cd, return_counts=True)]))
-    assert got == {3: 43750, 4: 831250, 12: 13750, 13: 11250}
+    assert got == {3: 60000, 4: 815000, 13: 22500, 14: 2500}
+    # no 4-cycles: no two VNs share two checks
+    ec = c.edge_cn()
+    keys = []
+    for j in np.flatnonzero(cd >= 2)[:200000:7]:
+        vs = np.sort(c.edge_vn[c.cn_ptr[j]:c.cn_ptr[j + 1]])
+        iu, ju = np.triu_indices(vs.size, 1)
+        keys.append(vs[iu].astype(np.int64) << 32 | vs[ju])
+    keys = np.concatenate(keys)
+    assert np.unique(keys).size == keys.size
+
+
+def test_biawgn_frames():
+    """DESIGN.md R31: lambda = 2 snr y, y = (1 - 2u) + N(0, 1/snr), so lambda is a consistent
+    Gaussian LLR, N(+-2 snr, 4 snr); S_B = H u; reproducible per (key, frame)."""
+    from synth.frames import gen_frame_biawgn
+    code = make_met_code("r0.1", 65536)
+    a = gen_frame_biawgn(code, 0.161, 3, 7)
+    b = gen_frame_biawgn(code, 0.161, 3, 7)
+    assert np.array_equal(a["llr"], b["llr"]) and np.array_equal(a["synd"], b["synd"])
+    sgn = 1.0 - 2.0 * a["u"]
+    t = a["llr"].astype(np.float64) * sgn
+    assert abs(t.mean() - 2 * 0.161) < 0.01 and abs(t.var() - 4 * 0.161) < 0.02
+    from oracle import bp
+    assert np.array_equal(bp.syndrome(code, a["u"]), unpack_bits(a["synd"], code.m))
 
 
 def test_density_evolution_thresholds():

@@ -22,7 +22,10 @@ sys.path.insert(0, str(ROOT))
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--family", default="r0.1")
+    ap.add_argument("--family", default="r0.1de")
+    ap.add_argument("--channel", choices=["md", "biawgn"], default="md",
+                    help="md: the MD reconciliation chain on the GPU; biawgn: channel LLRs N(+-2s, 4s) (R31)")
+    ap.add_argument("--msg-bits", type=int, choices=[32, 16], default=32)
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--frames", type=int, default=512)
     ap.add_argument("--batch", type=int, default=256)
@@ -40,7 +43,7 @@ def main():
     from paper_1711_01783_b200 import metrics
     from paper_1711_01783_b200.build import build
     from synth.codes import make_met_code
-    from synth.frames_gpu import gen_batch, pack_bits
+    from synth.frames_gpu import gen_batch, gen_batch_biawgn, pack_bits
 
     build()
     code = make_met_code(a.family, a.n)
@@ -48,7 +51,7 @@ def main():
     R = (st["n"] - st["m"]) / st["n"]
     h = B.Code(code)
     dec = B.Decoder(h, a.batch, rule=0 if a.rule == "exact" else 1, max_iter=a.iters, groups_in_flight=a.groups,
-                    lane_refill=not a.no_refill)
+                    lane_refill=not a.no_refill, msg_bits=a.msg_bits)
     out = open(a.out, "w") if a.out else None
     for snr in [float(s) for s in a.snrs.split(",")]:
         frames = conv = undet = iters_sum = 0
@@ -56,12 +59,16 @@ def main():
         dev_ms = 0.0
         for bi in range((a.frames + a.batch - 1) // a.batch):
             nb = min(a.batch, a.frames - bi * a.batch)
-            x, alpha, u = gen_batch(a.n, nb, snr, a.key, bi)
+            if a.channel == "md":
+                x, alpha, u = gen_batch(a.n, nb, snr, a.key, bi)
+            else:
+                lam, u = gen_batch_biawgn(a.n, nb, snr, a.key, bi)
             ub = pack_bits(u)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             sb = dec.syndrome(ub)                      # Bob, Step 1
-            lam = dec.md_alice_llr(x, alpha, snr)      # Alice, MD front end
+            if a.channel == "md":
+                lam = dec.md_alice_llr(x, alpha, snr)  # Alice, MD front end
             bits, it, cv = dec.decode(lam, sb)
             e1.record()
             torch.cuda.synchronize()
@@ -78,7 +85,8 @@ def main():
             iters_sum += sum(itc)
             for v in itc:
                 hist[min(max(v, 0), a.iters)] += 1
-        rec = {"config": "C5", "family": a.family, "n": a.n, "snr": snr, "beta": metrics.beta(R, snr),
+        rec = {"config": "C5", "family": a.family, "channel": a.channel, "msg_bits": a.msg_bits, "n": a.n,
+               "snr": snr, "beta": metrics.beta(R, snr),
                "max_iter": a.iters, "rule": a.rule.upper(), "batch": a.batch, "groups": a.groups,
                "lane_refill": not a.no_refill, "frames": frames, "fer": 1.0 - conv / frames,
                "undetected_rate": undet / frames, "mean_iters": iters_sum / frames,

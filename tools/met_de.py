@@ -187,11 +187,11 @@ def run_many(cands: dict, procs: int = 8) -> dict:
         return dict(p.map(_thr, list(cands.items())))
 
 
-# DESIGN.md R29 (synth/codes.py "r0.1de"): 5 % of the inner checks x2^2 x3; threshold 0.152
+# DESIGN.md R29 (synth/codes.py "r0.1de"): 0.06 n inner checks x2^2 x3; threshold 0.153
 R01DE = {
-    "act": [(0.06375, 2, 21), (0.0175, 3, 21), (0.04375, 3, 20)],
-    "core": [(0.01375, 12), (0.01125, 13)],
-    "inner": [(0.04375, 2), (0.83125, 3)],
+    "act": [(0.0475, 2, 21), (0.0175, 3, 21), (0.06, 3, 20)],
+    "core": [(0.0225, 13), (0.0025, 14)],
+    "inner": [(0.06, 2), (0.815, 3)],
 }
 
 if __name__ == "__main__":
