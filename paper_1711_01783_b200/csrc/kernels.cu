@@ -614,6 +614,9 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
 #ifndef METLDPC_RING_CW
 #define METLDPC_RING_CW 31      // compute warps of the CN ring kernel (+ 1 producer warp)
 #endif
+#ifndef METLDPC_RING_CW_CORE
+#define METLDPC_RING_CW_CORE 15 // compute warps of the ring kernel for classes with 5..16 active slots
+#endif
 #ifndef METLDPC_RING_STAGES
 #define METLDPC_RING_STAGES 6   // CTA ring depth cap (k_cn_ring)
 #endif
@@ -854,7 +857,9 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 
 template <int NA, int ND, int MSG>
 struct RingCfg {
-    static constexpr int CW = METLDPC_RING_CW;                        // compute warps = CNs per stage
+    // compute warps = CNs per stage: 64 registers for the inner classes (NA <= 4), up to 128 for
+    // the core classes (NA > 4, 16 warps per SM)
+    static constexpr int CW = NA <= 4 ? METLDPC_RING_CW : METLDPC_RING_CW_CORE;
     static constexpr int RB = MSG ? 128 : 256;                        // r row bytes (64 lanes)
     // word arrays are copied from the 16-byte-aligned word at or below the first one needed
     // (lead 0..3 words) and rounded up to 16 bytes; the device arrays are padded for it
@@ -1863,8 +1868,19 @@ static void* cn_pipe_kernel_m(int na, int nd) {
     return nullptr;
 }
 
+template <int RULE, int MSG, int NA = 5>
+static void* cn_ring_core_kernel(int na) {   // core classes: 5..16 active slots, no degree-1 slot
+    if constexpr (NA <= kMaxUnrolledCnDeg) {
+        if (na == NA) return reinterpret_cast<void*>(&k_cn_ring<RULE, NA, 0, MSG>);
+        return cn_ring_core_kernel<RULE, MSG, NA + 1>(na);
+    } else {
+        return nullptr;
+    }
+}
+
 template <int RULE, int MSG>
 static void* cn_ring_kernel_m(int na, int nd) {
+    if (na > 4) return nd == 0 ? cn_ring_core_kernel<RULE, MSG>(na) : nullptr;
     switch (na * 2 + nd) {
         case 2: return reinterpret_cast<void*>(&k_cn_ring<RULE, 1, 0, MSG>);
         case 3: return reinterpret_cast<void*>(&k_cn_ring<RULE, 1, 1, MSG>);
@@ -1895,8 +1911,20 @@ static void ring_geom(int* threads, size_t* smem) {
     *smem = size_t(RingCfg<NA, ND, MSG>::SMEM);
 }
 
+template <int MSG, int NA = 5>
+static void cn_ring_core_geom(int na, int* threads, size_t* smem) {
+    if constexpr (NA <= kMaxUnrolledCnDeg) {
+        if (na == NA) return ring_geom<NA, 0, MSG>(threads, smem);
+        return cn_ring_core_geom<MSG, NA + 1>(na, threads, smem);
+    } else {
+        *threads = 0;
+        *smem = 0;
+    }
+}
+
 template <int MSG>
 static void cn_ring_geom_m(int D, int nd, int* threads, size_t* smem) {
+    if (D - nd > 4) return cn_ring_core_geom<MSG>(D - nd, threads, smem);
     switch ((D - nd) * 2 + nd) {
         case 2: ring_geom<1, 0, MSG>(threads, smem); return;
         case 3: ring_geom<1, 1, MSG>(threads, smem); return;
@@ -1929,7 +1957,16 @@ bool cn_use_pipe(int D, int nd) {
         const char* e = std::getenv("METLDPC_PIPE");
         return !(e && e[0] == '0');
     }();
-    return on && D >= 0 && nd <= 1 && D - nd >= 1 && D - nd <= 4;
+    // core classes (5..16 active slots, no degree-1 slot) in the ring kernel too (default;
+    // METLDPC_RING_CORE=0: the register-only tiled kernel).  Measured (r0.1de C3, fixed N, same
+    // call): CN phase fp32 0.463 vs 0.473 ms, 16-bit 0.378 vs 0.393 ms.
+    static const bool core = [] {
+        const char* e = std::getenv("METLDPC_RING_CORE");
+        return !(e && e[0] == '0');
+    }();
+    if (!on || D < 0 || nd > 1 || D - nd < 1) return false;
+    if (D - nd <= 4) return true;
+    return core && cn_use_ring() && nd == 0 && D <= kMaxUnrolledCnDeg;
 }
 
 template <int NA, int ND, int MSG>
