@@ -340,11 +340,12 @@ __device__ __forceinline__ uint32_t msg16_pack(float2 o) {
 // MSG = 0: r rows of fp32 (pr: float row pointer, ro: the messages).  MSG = 1: 16-bit rows
 // (pr: the thread's word of the row as uint32_t*, ro: the integers q of the stored messages,
 // x = fmaf(q, -2^-10, L) = the single rounding of L - q 2^-10, N7).
-template <int RULE, int NA, int ND, int MSG = 0>
+// on = false (PRED only): compute but store nothing (the idle half-warp of a tail stage).
+template <int RULE, int NA, int ND, int MSG = 0, bool PRED = false>
 __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 0 ? NA : 1],
                                          const float2 (&ro)[NA > 0 ? NA : 1], float2 lam, uint2 sbit, uint2 d1prev,
                                          void* prv, float* pla, const uint32_t (&offs)[NA > 0 ? NA : 1],
-                                         uint2& d1bit) {
+                                         uint2& d1bit, bool on = true) {
     float* pr = static_cast<float*>(prv);
     constexpr int D = NA + ND;
     const uint32_t one = one_bits();
@@ -392,7 +393,7 @@ __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 
         const float2 o = make_float2(
             __uint_as_float(__float_as_uint(fminf(ph.x, kRMax)) | ((par0 ^ xb0[s]) & 0x80000000u)),
             __uint_as_float(__float_as_uint(fminf(ph.y, kRMax)) | ((par1 ^ xb1[s]) & 0x80000000u)));
-        if (s < NA) {
+        if (s < NA && (!PRED || on)) {
             // Unpredicated: a latched or padding lane's r and accumulator columns are never
             // read for that lane again (k_finish keeps its L and clears the accumulator), and
             // full 256-byte rows avoid partial-sector writes.
@@ -613,6 +614,9 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
 #endif
 #ifndef METLDPC_RING_CW
 #define METLDPC_RING_CW 31      // compute warps of the CN ring kernel (+ 1 producer warp)
+#endif
+#ifndef METLDPC_RING_CW2
+#define METLDPC_RING_CW2 19     // compute warps of the two-CNs-per-warp ring kernel (~100 registers)
 #endif
 #ifndef METLDPC_RING_CW_CORE
 #define METLDPC_RING_CW_CORE 15 // compute warps of the ring kernel for classes with 5..16 active slots
@@ -855,19 +859,27 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+#ifndef METLDPC_RING_CPW
+#define METLDPC_RING_CPW 1      // CNs per compute warp of the inner-class ring kernel (1, or 2 = one per half-warp)
+#endif
+
 template <int NA, int ND, int MSG>
 struct RingCfg {
+    // CNs per compute warp: 2 = one CN per half-warp, each thread four lanes (two fp32 pairs),
+    // so the per-CN overhead is shared by two CNs (inner classes only)
+    static constexpr int CPW = NA <= 4 ? METLDPC_RING_CPW : 1;
     // compute warps = CNs per stage: 64 registers for the inner classes (NA <= 4), up to 128 for
     // the core classes (NA > 4, 16 warps per SM)
-    static constexpr int CW = NA <= 4 ? METLDPC_RING_CW : METLDPC_RING_CW_CORE;
+    static constexpr int CW = NA <= 4 ? (CPW == 2 ? METLDPC_RING_CW2 : METLDPC_RING_CW) : METLDPC_RING_CW_CORE;
+    static constexpr int SC = CW * CPW;                               // CNs per stage
     static constexpr int RB = MSG ? 128 : 256;                        // r row bytes (64 lanes)
     // word arrays are copied from the 16-byte-aligned word at or below the first one needed
     // (lead 0..3 words) and rounded up to 16 bytes; the device arrays are padded for it
-    static constexpr int IDX_BYTES = ((CW * NA + 8) * 4 + 15) / 16 * 16;
-    static constexpr int W_BYTES = ((CW * 2 + 8) * 4 + 15) / 16 * 16;
+    static constexpr int IDX_BYTES = ((SC * NA + 8) * 4 + 15) / 16 * 16;
+    static constexpr int W_BYTES = ((SC * 2 + 8) * 4 + 15) / 16 * 16;
     static constexpr int OFF_R = 0;
-    static constexpr int OFF_L1 = OFF_R + CW * NA * RB;
-    static constexpr int OFF_IDX = OFF_L1 + ND * CW * 256;
+    static constexpr int OFF_L1 = OFF_R + SC * NA * RB;
+    static constexpr int OFF_IDX = OFF_L1 + ND * SC * 256;
     static constexpr int OFF_SY = OFF_IDX + IDX_BYTES;
     static constexpr int OFF_D1 = OFF_SY + W_BYTES;
     static constexpr int STG = OFF_D1 + ND * W_BYTES;
@@ -896,7 +908,8 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
     k_cn_ring(CodeDev cd, Group g, CnCtl karg, int begin, int count) {
     using PT = PhiT<RULE>;
     using RC = RingCfg<NA, ND, MSG>;
-    constexpr int CW = RC::CW, S = RC::STAGES;
+    constexpr int CW = RC::CW, S = RC::STAGES, SC = RC::SC, CPW = RC::CPW;
+    constexpr int NP = CPW == 2 ? 2 : 1;           // lane pairs per thread
     extern __shared__ __align__(16) char smem[];
     __shared__ uint32_t s_unsat[2], s_act[2], s_fresh[2];
     pdl_launch_dependents();
@@ -923,18 +936,17 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
     }
     const int abase = __ldg(cd.cn_aptr + begin);
     const int dbase = ND ? __ldg(cd.cn_dptr + begin) : 0;
-    const int nst = (count + CW - 1) / CW;
+    const int nst = (count + SC - 1) / SC;
     const bool d1in = ND > 0 && k.check;           // degree-1 decisions of l - 1 for the syndrome test
     load_phi_table<RULE>(smem, cd.phi);
     __syncthreads();
-    uint32_t un0 = 0, un1 = 0;
-    if (warp == CW) {
+    if (warp == CW) {                              // ---- producer warp
         if (lane == 0) {
             const uint64_t pol = l2_evict_first_policy();
             int slot = 0, use = 0;
             for (int gs = blockIdx.x; gs < nst; gs += gridDim.x) {
                 if (use) mbar_wait(empty_a + 8 * slot, (use - 1) & 1);
-                const int j0 = gs * CW, ncn = min(CW, count - j0);
+                const int j0 = gs * SC, ncn = min(SC, count - j0);
                 const uint32_t dst = ring_a + slot * RC::STG, bar = full_a + 8 * slot;
                 const long wi = long(abase) + long(j0) * NA, ws = (long(begin) + j0) * 2,
                            wd = (long(k.rpar) * cd.n_1 + dbase + j0) * 2;
@@ -955,65 +967,96 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
                 }
             }
         }
-    } else {                                       // ---- compute warps: CN `warp` of every stage
+    } else {                                       // ---- compute warps: CN(s) `warp` of every stage
         const uint32_t tabk = phi_tab_lane<RULE>(smem, lane);
         const uint32_t am0 = s_act[0], am1 = s_act[1];
         const bool any_fresh = (s_fresh[0] | s_fresh[1]) != 0u;
-        const bool f0 = (s_fresh[0] >> lane) & 1u, f1 = (s_fresh[1] >> lane) & 1u;
+        // CPW = 1: the thread's lanes are (lane, lane + 32); CPW = 2: half-warp h takes CN 2 w + h,
+        // thread t = lane & 15 its lanes (t, t + 32) and (t + 16, t + 48)
+        const int sub = CPW == 2 ? (lane >> 4) : 0;
+        const int t0 = CPW == 2 ? (lane & 15) : lane;
+        uint32_t un0[NP], un1[NP];
+#pragma unroll
+        for (int q = 0; q < NP; ++q) un0[q] = un1[q] = 0u;
         int slot = 0;
         uint32_t phase = 0;   // parity of the slot's current use
         for (int gs = blockIdx.x; gs < nst; gs += gridDim.x) {
-            const int j0 = gs * CW, ncn = min(CW, count - j0);
+            const int j0 = gs * SC, ncn = min(SC, count - j0);
             mbar_wait(full_a + 8 * slot, phase);
-            if (warp < ncn) {
+            if (warp * CPW < ncn) {
+                const int cw = warp * CPW + sub;          // CN of this (half-)warp within the stage
+                const bool on = CPW == 1 || cw < ncn;     // (CPW = 1: the warp test above)
+                const int cwc = (CPW == 1 || on) ? cw : cw - 1;   // an idle tail half reads its sibling's CN, stores nothing
                 const char* sp = ring + slot * RC::STG;
-                const int jl = j0 + warp;
-                const int* sidx = reinterpret_cast<const int*>(sp + RC::OFF_IDX) + ((abase + j0 * NA) & 3) + warp * NA;
-                uint32_t offs[NA];
-                float2 L2[NA], r2[NA];
-#pragma unroll
-                for (int s = 0; s < NA; ++s) {
-                    offs[s] = uint32_t(sidx[s]) * 128u + uint32_t(lane);
-                    L2[s] = make_float2(__ldg(g.L + offs[s]), __ldg(g.L + offs[s] + 32));   // L2-resident gathers
-                }
-                const uint32_t* ssy = reinterpret_cast<const uint32_t*>(sp + RC::OFF_SY) + (((begin + j0) * 2) & 3) + warp * 2;
+                const int jl = j0 + cwc;
+                const int* sidx = reinterpret_cast<const int*>(sp + RC::OFF_IDX) + ((abase + j0 * NA) & 3) + cwc * NA;
+                const uint32_t* ssy = reinterpret_cast<const uint32_t*>(sp + RC::OFF_SY) + (((begin + j0) * 2) & 3) + cwc * 2;
                 const uint32_t swx = ssy[0], swy = ssy[1];
                 uint2 wv = make_uint2(0, 0);
                 if constexpr (ND > 0)
                     if (d1in) {
                         const uint32_t* sd =
-                            reinterpret_cast<const uint32_t*>(sp + RC::OFF_D1) + ((long(k.rpar) * cd.n_1 + dbase + j0) * 2 & 3) + warp * 2;
+                            reinterpret_cast<const uint32_t*>(sp + RC::OFF_D1) + ((long(k.rpar) * cd.n_1 + dbase + j0) * 2 & 3) + cwc * 2;
                         wv = make_uint2(sd[0], sd[1]);
                     }
-                const float* sr = reinterpret_cast<const float*>(sp + RC::OFF_R + warp * NA * RC::RB);
+                const float* sr = reinterpret_cast<const float*>(sp + RC::OFF_R + cwc * NA * RC::RB);
+                const float* sl = reinterpret_cast<const float*>(sp + RC::OFF_L1 + cwc * 256);
+                uint32_t bx[NP], by[NP];   // ballots of the degree-1 decisions, per pair
 #pragma unroll
-                for (int s = 0; s < NA; ++s) {
-                    if constexpr (MSG) r2[s] = msg16_q(reinterpret_cast<const uint32_t*>(sr)[s * 32 + lane]);
-                    else r2[s] = make_float2(sr[s * 64 + lane], sr[s * 64 + 32 + lane]);
-                }
-                if (any_fresh) {   // r^0 = 0 for a frame starting in this pass (Step 2), in registers
+                for (int q = 0; q < NP; ++q) {
+                    const int base = t0 + 16 * q;         // the pair's first lane (second: base + 32)
+                    uint32_t offs[NA];
+                    float2 L2[NA], r2[NA];
 #pragma unroll
                     for (int s = 0; s < NA; ++s) {
-                        if (f0) r2[s].x = 0.0f;
-                        if (f1) r2[s].y = 0.0f;
+                        offs[s] = uint32_t(sidx[s]) * 128u + uint32_t(base);
+                        L2[s] = make_float2(__ldg(g.L + offs[s]), __ldg(g.L + offs[s] + 32));   // L2-resident gathers
+                    }
+#pragma unroll
+                    for (int s = 0; s < NA; ++s) {
+                        if constexpr (MSG) r2[s] = msg16_q(reinterpret_cast<const uint32_t*>(sr)[s * 32 + base]);
+                        else r2[s] = make_float2(sr[s * 64 + base], sr[s * 64 + 32 + base]);
+                    }
+                    if (any_fresh) {   // r^0 = 0 for a frame starting in this pass (Step 2), in registers
+                        const bool f0 = (s_fresh[0] >> base) & 1u, f1 = (s_fresh[1] >> base) & 1u;
+#pragma unroll
+                        for (int s = 0; s < NA; ++s) {
+                            if (f0) r2[s].x = 0.0f;
+                            if (f1) r2[s].y = 0.0f;
+                        }
+                    }
+                    float2 lam = make_float2(0.0f, 0.0f);
+                    if constexpr (ND > 0) lam = make_float2(sl[base], sl[32 + base]);
+                    void* pr = MSG ? static_cast<void*>(reinterpret_cast<unsigned int*>(g.r) + (size_t(abase + jl * NA) * 32 + base))
+                                   : static_cast<void*>(g.r + (size_t(abase + jl * NA) * 64 + base));
+                    uint2 d1 = make_uint2(0, 0);
+                    const uint2 c2 = cn_pair<RULE, NA, ND, MSG, (CPW == 2)>(
+                        tabk, L2, r2, lam, make_uint2((swx >> base) & 1u, (swy >> base) & 1u),
+                        make_uint2((wv.x >> base) & 1u, (wv.y >> base) & 1u), pr, g.L, offs, d1, on);
+                    // syndrome-test flags of the lanes (CPW = 2: folded into 32-lane words at the end)
+                    un0[q] |= __ballot_sync(FULL, CPW == 1 ? c2.x : (c2.x && on));
+                    un1[q] |= __ballot_sync(FULL, CPW == 1 ? c2.y : (c2.y && on));
+                    if constexpr (ND > 0) {
+                        bx[q] = __ballot_sync(FULL, d1.x);
+                        by[q] = __ballot_sync(FULL, d1.y);
                     }
                 }
-                float2 lam = make_float2(0.0f, 0.0f);
                 if constexpr (ND > 0) {
-                    const float* sl = reinterpret_cast<const float*>(sp + RC::OFF_L1 + warp * 256);
-                    lam = make_float2(sl[lane], sl[32 + lane]);
-                }
-                void* pr = MSG ? static_cast<void*>(reinterpret_cast<unsigned int*>(g.r) + (size_t(abase + jl * NA) * 32 + lane))
-                               : static_cast<void*>(g.r + (size_t(abase + jl * NA) * 64 + lane));
-                uint2 d1 = make_uint2(0, 0);
-                const uint2 c2 = cn_pair<RULE, NA, ND, MSG>(tabk, L2, r2, lam,
-                                                            make_uint2((swx >> lane) & 1u, (swy >> lane) & 1u),
-                                                            make_uint2((wv.x >> lane) & 1u, (wv.y >> lane) & 1u), pr, g.L, offs, d1);
-                un0 |= __ballot_sync(FULL, c2.x);
-                un1 |= __ballot_sync(FULL, c2.y);
-                if constexpr (ND > 0) {
-                    uint2 b = make_uint2(__ballot_sync(FULL, d1.x), __ballot_sync(FULL, d1.y));
-                    if (lane == 0) {
+                    uint2 b;
+                    if constexpr (CPW == 2) {   // pair q of half h holds lanes 16 q + t of CN 2 w + h
+                        uint32_t x, y;
+                        if (sub == 0) {
+                            asm("prmt.b32 %0, %1, %2, 0x5410;" : "=r"(x) : "r"(bx[0]), "r"(bx[1]));
+                            asm("prmt.b32 %0, %1, %2, 0x5410;" : "=r"(y) : "r"(by[0]), "r"(by[1]));
+                        } else {
+                            asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(x) : "r"(bx[0]), "r"(bx[1]));
+                            asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(y) : "r"(by[0]), "r"(by[1]));
+                        }
+                        b = make_uint2(x, y);
+                    } else {
+                        b = make_uint2(bx[0], by[0]);
+                    }
+                    if (t0 == 0 && (CPW == 1 || on)) {
                         uint2* wp = reinterpret_cast<uint2*>(g.d1bits) + (size_t(k.wpar) * cd.n_1 + dbase + jl);
                         if ((am0 & am1) != FULL) {   // keep the words of lanes not iterating
                             const uint2 o = *wp;
@@ -1031,9 +1074,17 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
                 phase ^= 1u;
             }
         }
+        uint32_t u0, u1;
+        if constexpr (CPW == 2) {   // bit 16 h + t of pair q's ballot = lane 16 q + t of a CN
+            u0 = ((un0[0] | (un0[0] >> 16)) & 0xFFFFu) | ((un0[1] | (un0[1] << 16)) & 0xFFFF0000u);
+            u1 = ((un1[0] | (un1[0] >> 16)) & 0xFFFFu) | ((un1[1] | (un1[1] << 16)) & 0xFFFF0000u);
+        } else {
+            u0 = un0[0];
+            u1 = un1[0];
+        }
         if (k.check && lane == 0) {
-            if (un0 & am0) atomicOr(&s_unsat[0], un0 & am0);
-            if (un1 & am1) atomicOr(&s_unsat[1], un1 & am1);
+            if (u0 & am0) atomicOr(&s_unsat[0], u0 & am0);
+            if (u1 & am1) atomicOr(&s_unsat[1], u1 & am1);
         }
     }
     __syncthreads();
