@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
 #define METLDPC_PIPE_WARPS 32   // warps per CTA cap (at most what the rings leave room for)
 #endif
 #ifndef METLDPC_RING_CW
-#define METLDPC_RING_CW 31      // compute warps of the CN ring kernel (+ 1 producer warp)
+#define METLDPC_RING_CW 23      // compute warps of the CN ring kernel (+ 1 producer warp; 80 registers)
 #endif
 #ifndef METLDPC_RING_CW2
 #define METLDPC_RING_CW2 19     // compute warps of the two-CNs-per-warp ring kernel (~100 registers)

@@ -14,8 +14,8 @@ structural count of Table 1 exactly at n = 10^6:
   n=10^6: E = 3,480,000, m = 950,000, 930,000 degree-1 VNs, E_it = 2,550,000.
 * ``r0.1de`` (R29): the same Table-1 counts with degrees chosen by density
   evolution (tools/met_de.py) and finite-length runs (tools/met_search.py):
-  nu = 0.0475 x1^2 x2^21 + 0.0175 x1^3 x2^21 + 0.06 x1^3 x2^20 + 0.875 x3,
-  mu = 0.0225 x1^13 + 0.0025 x1^14 + 0.06 x2^2 x3 + 0.815 x2^3 x3, built without 4-cycles
+  nu = 0.05 x1^2 x2^21 + 0.0175 x1^3 x2^21 + 0.0575 x1^3 x2^20 + 0.875 x3,
+  mu = 0.025 x1^13 + 0.0575 x2^2 x3 + 0.8175 x2^3 x3, built without 4-cycles
   among the active VNs (DE threshold SNR 0.153 vs 0.182 for ``r0.1``).
 * ``r0.02`` (R25): nu = 0.02 x1^2 x2^{56|57} + 0.02 x1^3 x2^{56|57} + 0.96 x3,
   mu = 0.02 x1^5 + 0.6025 x2^2 x3 + 0.3575 x2^3 x3 (inner degree 57 on 37,500 of the 40,000
@@ -127,16 +127,17 @@ def met_counts(family: str, n: int) -> dict:
     elif family == "r0.1de":
         # DESIGN.md R29 / SURVEY 8(f) #4: same Table-1 counts (n_1 = 7n/8, m = n - 0.1 n,
         # E_it = 2.8925 n, one degree-1 VN per inner check), degrees chosen by density evolution
-        # (tools/met_de.py) and finite-length runs (tools/met_search.py): 0.06 n inner checks
-        # x2^2 x3, the rest x2^3 x3; the remaining iterating edges go to the core (VN core
-        # degrees 2/3, check degrees 13/14); inner VN degrees 20/21; no 4-cycles among the
-        # active VNs (make_met_code).  DE threshold SNR 0.153 on the BIAWGN channel (r0.1: 0.182).
+        # (tools/met_de.py) and finite-length runs (tools/met_search.py): 0.0575 n inner checks
+        # x2^2 x3, the rest x2^3 x3, which leaves exactly 13 x (m - n_1) core edges: every core
+        # check has degree 13 (one kernel class); VN core degrees 2/3, inner VN degrees 20/21;
+        # no 4-cycles among the active VNs (make_met_code).  DE threshold SNR 0.153 on the
+        # BIAWGN channel (r0.1: 0.182).
         if n % 8:
             raise ValueError("r0.1de stand-in needs n divisible by 8")
         a = n // 8
         n1 = 7 * n // 8
         m = n - int(round(0.1 * n))
-        t2 = int(round(0.06 * n))
+        t2 = int(round(0.0575 * n))
         inner = {2: t2, 3: n1 - t2}
         e2 = 2 * t2 + 3 * (n1 - t2)
         e1 = int(round(2.8925 * n)) - e2

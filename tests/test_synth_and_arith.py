@@ -67,10 +67,10 @@ def test_r01de_degree_structure():
     c = make_met_code("r0.1de", 10 ** 6)
     vd, cd = c.vn_degree, c.cn_degree
     got = dict(zip(*[x.tolist() for x in np.unique(vd, return_counts=True)]))
-    # active VNs: (core 2, inner 21) 47,500 -> 23; (3, 21) 17,500 -> 24; (3, 20) 60,000 -> 23
-    assert got == {1: 875000, 23: 47500 + 60000, 24: 17500}
+    # active VNs: (core 2, inner 21) 50,000 -> 23; (3, 21) 17,500 -> 24; (3, 20) 57,500 -> 23
+    assert got == {1: 875000, 23: 50000 + 57500, 24: 17500}
     got = dict(zip(*[x.tolist() for x in np.unique(cd, return_counts=True)]))
-    assert got == {3: 60000, 4: 815000, 13: 22500, 14: 2500}
+    assert got == {3: 57500, 4: 817500, 13: 25000}
     # no 4-cycles: no two VNs share two checks
     ec = c.edge_cn()
     keys = []

@@ -187,11 +187,12 @@ def run_many(cands: dict, procs: int = 8) -> dict:
         return dict(p.map(_thr, list(cands.items())))
 
 
-# DESIGN.md R29 (synth/codes.py "r0.1de"): 0.06 n inner checks x2^2 x3; threshold 0.153
+# DESIGN.md R29 (synth/codes.py "r0.1de"): 0.0575 n inner checks x2^2 x3, every core check
+# degree 13; threshold 0.153
 R01DE = {
-    "act": [(0.0475, 2, 21), (0.0175, 3, 21), (0.06, 3, 20)],
-    "core": [(0.0225, 13), (0.0025, 14)],
-    "inner": [(0.06, 2), (0.815, 3)],
+    "act": [(0.05, 2, 21), (0.0175, 3, 21), (0.0575, 3, 20)],
+    "core": [(0.025, 13)],
+    "inner": [(0.0575, 2), (0.8175, 3)],
 }
 
 if __name__ == "__main__":
