@@ -457,10 +457,13 @@ def main():
     tpath = ROOT / "profiles" / "cn_traffic.json"
     if tpath.exists():
         try:
-            tj = json.loads(tpath.read_text())
-            w = tj.get("workload", {})
-            if (w.get("family"), w.get("n"), w.get("no_skip", False), w.get("lanes", 64), w.get("rule", "exact"),
-                    w.get("msg_bits", 32)) == (a.family, a.n, bool(a.no_skip), a.lanes, a.rule, a.msg_bits):
+            tj_all = json.loads(tpath.read_text())
+            for tj in (tj_all if isinstance(tj_all, list) else [tj_all]):
+                w = tj.get("workload", {})
+                if (w.get("family"), w.get("n"), w.get("no_skip", False), w.get("lanes", 64),
+                        str(w.get("rule", "exact")).lower(), w.get("msg_bits", 32)) != \
+                        (a.family, a.n, bool(a.no_skip), a.lanes, a.rule, a.msg_bits):
+                    continue
                 traffic = tj.get("dram_bytes_per_launch")
                 pg = tj.get("production_graph", {})
                 traffic_prod = pg.get("dram_bytes_per_pass")
@@ -469,6 +472,7 @@ def main():
                     # production pass (same capture), against the same peak
                     traffic_prod = {"bytes": traffic_prod, "ms": pg["graph_ms_per_pass"],
                                     "dram_gbs": traffic_prod / pg["graph_ms_per_pass"] / 1e6}
+                break
         except Exception:
             traffic = traffic_prod = None
     # codeword-iterations the timed steps decoded: the counters' sum of iterations over valid
@@ -478,7 +482,7 @@ def main():
                 "frac": (cn_gbs / peak) if cn_gbs else None, "traffic": traffic,
                 "traffic_production_pass": (dict(traffic_prod, frac=traffic_prod["dram_gbs"] / peak)
                                             if isinstance(traffic_prod, dict) and peak else traffic_prod),
-                "kernel": "CN phase: k_cn_pipe + k_cn_tile launches of one iteration (all degree classes, VN sums fused)",
+                "kernel": "CN phase: the k_cn_ring launches of one iteration (all degree classes, VN sums fused)",
                 "bytes_per_launch": bm["cn"] * min(F, a.lanes),
                 "bytes_model": f"2 E_it s_r + 4 (n_1 + n_a) + m/8 per codeword-iteration, s_r = {a.msg_bits // 8} "
                                "(SURVEY 8(d) without the VN write-back, which the fused VN sum keeps in L2), x 64 lanes",
