@@ -70,7 +70,7 @@ def parse():
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--snr", type=float, default=0.161)
     ap.add_argument("--iters", type=int, default=100)
-    ap.add_argument("--frames", type=int, default=2048,
+    ap.add_argument("--frames", type=int, default=4096,
                     help="frames per GPU per step (a streaming decode's fill and drain, about one frame's "
                          "decoding time, is amortised over the batch)")
     ap.add_argument("--distinct", type=int, default=64, help="distinct frames generated per rank (tiled)")

@@ -1058,12 +1058,19 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
                     }
                     if (t0 == 0 && (CPW == 1 || on)) {
                         uint2* wp = reinterpret_cast<uint2*>(g.d1bits) + (size_t(k.wpar) * cd.n_1 + dbase + jl);
-                        if ((am0 & am1) != FULL) {   // keep the words of lanes not iterating
-                            const uint2 o = *wp;
-                            b.x = (b.x & am0) | (o.x & ~am0);
-                            b.y = (b.y & am1) | (o.y & ~am1);
+                        if ((am0 & am1) != FULL) {
+                            // keep the words of lanes not iterating, without a read on the warp's path:
+                            // AND clears the iterating lanes' 0 bits, OR sets their 1 bits (two
+                            // fire-and-forget reductions, applied in order; the words are read again
+                            // only by the next pass)
+                            unsigned int* w = reinterpret_cast<unsigned int*>(wp);
+                            atomicAnd(w, b.x | ~am0);
+                            atomicOr(w, b.x & am0);
+                            atomicAnd(w + 1, b.y | ~am1);
+                            atomicOr(w + 1, b.y & am1);
+                        } else {
+                            *wp = b;
                         }
-                        *wp = b;
                     }
                 }
             }
@@ -1598,28 +1605,35 @@ __global__ void __launch_bounds__(256) k_finalize_lanes(CodeDev cd, Group g, Str
     const int b = c * 32 + lane;
     const bool mine = (g.fin[c] >> lane) & 1u;
     const int f = mine ? g.lane_frame[b] : -1;
-    if (f < 0) return;
-    const int it = g.iters[b];
-    if (blockIdx.x == 0 && threadIdx.x < 32) {
+    if (__ballot_sync(FULL, f >= 0) == 0u || wblk >= NW) {   // warp-uniform exits
+        if (f >= 0 && blockIdx.x == 0 && threadIdx.x < 32) {
+            job->iters[f] = g.iters[b];
+            job->conv[f] = g.conv[b];
+        }
+        return;
+    }
+    const int it = f >= 0 ? g.iters[b] : 0;
+    if (f >= 0 && blockIdx.x == 0 && threadIdx.x < 32) {
         job->iters[f] = it;
         job->conv[f] = g.conv[b];
     }
-    if (wblk >= NW) return;
     const size_t off = size_t(c) * 32 + lane;
-    const int par = g.lane_fbuf[b];
-    uint32_t word = 0;
+    const int par = f >= 0 ? g.lane_fbuf[b] : 0;
     const int i0 = wblk * 32;
+    // the word's 32 VN indices in one coalesced load, then 32 independent loads in flight
+    const int vm = (i0 + lane < cd.n) ? __ldg(cd.vmap + i0 + lane) : 0;
+    uint32_t word = 0;
+#pragma unroll
     for (int ii = 0; ii < 32; ++ii) {
-        const int i = i0 + ii;
-        if (i >= cd.n) break;
-        const int v = __ldg(cd.vmap + i);
-        uint32_t bit;
-        if (v >= 0) bit = g.L[size_t(v) * 2 * g.B + off] < 0.0f;
-        else bit = (g.d1bits[(size_t(par) * cd.n_1 + ~v) * g.C + c] >> lane) & 1u;
+        const int v = __shfl_sync(FULL, vm, ii);
+        uint32_t bit = 0;
+        if (f >= 0 && i0 + ii < cd.n) {
+            if (v >= 0) bit = g.L[size_t(v) * 2 * g.B + off] < 0.0f;
+            else bit = (g.d1bits[(size_t(par) * cd.n_1 + ~v) * g.C + c] >> lane) & 1u;
+        }
         word |= bit << ii;
     }
-    if (it < 0) word = 0;
-    job->bits[size_t(f) * NW + wblk] = word;
+    if (f >= 0) job->bits[size_t(f) * NW + wblk] = (it < 0) ? 0u : word;
 }
 
 // Refill wave 2/4: the finished lanes take the next frames of the queue (in lane order),
