@@ -1695,32 +1695,46 @@ __global__ void __launch_bounds__(256) k_refill_scatter(CodeDev cd, Group g, Str
     const int c = blockIdx.y;
     const uint32_t nm = g.newm[c];
     if (!nm) return;
-    const int i0 = blockIdx.x * 32;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int rr = w; rr < 32; rr += 8) {
-        const int f = ((nm >> rr) & 1u) ? g.lane_frame[c * 32 + rr] : -1;
-        const int i = i0 + lane;
-        tile[rr][lane] = (f >= 0 && i < cd.n) ? __ldcv(job->llr + size_t(f) * cd.n + i) : 0.0f;
-    }
-    __syncthreads();
     const size_t off = size_t(c) * 32 + lane;
     const bool mine = (nm >> lane) & 1u;
-    for (int ii = w; ii < 32; ii += 8) {
-        const int i = i0 + ii;
-        if (i >= cd.n) break;
-        const float val = tile[lane][ii];
-        const uint32_t bad = __ballot_sync(FULL, mine && !isfinite(val));
-        if (bad && lane == 0) atomicOr(g.invalid + c, bad);
-        if (!mine) continue;
-        const int v = __ldg(cd.vmap + i);
-        if (v >= 0) {
-            const float lz = __fadd_rn(val, 0.0f);      // -0 -> +0, as k_scatter
-            g.lam_a[size_t(v) * g.B + off] = lz;
-            g.L[size_t(v) * 2 * g.B + off] = lz;
-            g.L[size_t(v) * 2 * g.B + g.B + off] = 0.0f;
-        } else {
-            g.lam1[size_t(~v) * g.B + off] = lam1_phi_form(cd, val);
+    // frames of the new lanes (warp w reads rows w, w + 8, ...; rows of other lanes stay 0)
+    int fr[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int rr = w + 8 * q;
+        fr[q] = ((nm >> rr) & 1u) ? g.lane_frame[c * 32 + rr] : -1;
+    }
+    const int ntiles = (cd.n + 31) / 32;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {   // a few tiles of 32 VNs per block
+        const int i0 = t * 32;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int i = i0 + lane;
+            tile[w + 8 * q][lane] = (fr[q] >= 0 && i < cd.n) ? __ldcv(job->llr + size_t(fr[q]) * cd.n + i) : 0.0f;
         }
+        // the tile's VN indices: one coalesced load, broadcast by shuffles
+        const int vm = (i0 + lane < cd.n) ? __ldg(cd.vmap + i0 + lane) : 0;
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int ii = w + 8 * q, i = i0 + ii;
+            const int v = __shfl_sync(FULL, vm, ii);
+            if (i >= cd.n) break;
+            const float val = tile[lane][ii];
+            const uint32_t bad = __ballot_sync(FULL, mine && !isfinite(val));
+            if (bad && lane == 0) atomicOr(g.invalid + c, bad);
+            if (!mine) continue;
+            if (v >= 0) {
+                const float lz = __fadd_rn(val, 0.0f);      // -0 -> +0, as k_scatter
+                g.lam_a[size_t(v) * g.B + off] = lz;
+                g.L[size_t(v) * 2 * g.B + off] = lz;
+                g.L[size_t(v) * 2 * g.B + g.B + off] = 0.0f;
+            } else {
+                g.lam1[size_t(~v) * g.B + off] = lam1_phi_form(cd, val);
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -2159,7 +2173,7 @@ void launch_refill_wave(const CodeDev& cd, const Group& g, StreamJob* job, cudaS
     const int NW = (cd.n + 31) / 32, W = (cd.m + 31) / 32;
     k_finalize_lanes<<<dim3((NW + 7) / 8, g.C), 256, 0, s>>>(cd, g, job);
     k_refill_assign<<<1, 128, 0, s>>>(g, job);
-    k_refill_scatter<<<dim3((cd.n + 31) / 32, g.C), 256, 0, s>>>(cd, g, job);
+    k_refill_scatter<<<dim3(std::min((cd.n + 31) / 32, 148 * 8), g.C), 256, 0, s>>>(cd, g, job);
     k_refill_synd<<<unsigned((long(W) * g.C + 7) / 8), 256, 0, s>>>(cd, g, job);
     k_refill_activate<<<1, 128, 0, s>>>(g);
 }
