@@ -415,6 +415,46 @@ __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 
     return make_uint2((lw0 >> 31) ^ sbit.x ^ d1prev.x, (lw1 >> 31) ^ sbit.y ^ d1prev.y);
 }
 
+// DESIGN.md N1 for one CN and ONE lane, no degree-1 slot (the core classes of the half-warp ring
+// path): the element-wise operations of cn_pair in the same order.  MSG = 1: ro holds the integers q
+// of the 16-bit stored messages and prv the lane's half-word of the first r row.
+template <int RULE, int NA, int MSG>
+__device__ __forceinline__ uint32_t cn_one(uint32_t tabk, const float (&Lv)[NA], const float (&ro)[NA], uint32_t sbit,
+                                           void* prv, float* pla, const uint32_t (&offs)[NA]) {
+    const uint32_t one = one_bits();
+    float p[NA], P[NA];
+    uint32_t xb[NA];
+    uint32_t par = sbit << 31, lw = 0;
+#pragma unroll
+    for (int s = 0; s < NA; ++s) {
+        const float x = MSG ? __fmaf_rn(ro[s], -0.0009765625f, Lv[s]) : __fsub_rn(Lv[s], ro[s]);   // q = L - r (R10)
+        lw ^= __float_as_uint(Lv[s]);
+        xb[s] = __float_as_uint(x);
+        par ^= xb[s];
+        p[s] = phi_dev<RULE>(tabk, fabsf(x), one);
+    }
+    P[0] = 0.0f;
+    if constexpr (NA > 1) P[1] = p[0];
+#pragma unroll
+    for (int s = 2; s < NA; ++s) P[s] = __fadd_rn(P[s - 1], p[s - 1]);
+    float Q = 0.0f;
+#pragma unroll
+    for (int s = NA - 1; s >= 0; --s) {
+        const float S = (s == NA - 1) ? P[s] : (s == 0 ? Q : __fadd_rn(P[s], Q));
+        const float mag = fminf(phi_dev<RULE>(tabk, S, one), kRMax);
+        const float o = __uint_as_float(__float_as_uint(mag) | ((par ^ xb[s]) & 0x80000000u));
+        if constexpr (MSG) {
+            const uint32_t w = __float_as_uint(__fmaf_rn(o, 1024.0f, kMsg16Magic));   // stored message (N7)
+            __stcs(static_cast<unsigned short*>(prv) + s * 64, (unsigned short)(w & 0xFFFFu));
+        } else {
+            __stcs(static_cast<float*>(prv) + s * 64, o);
+        }
+        atomicAdd(reinterpret_cast<unsigned int*>(pla + offs[s] + 64), vn_fix(o));   // VN sum (Eq. 4, N3)
+        if (s > 0) Q = __fadd_rn(Q, p[s]);
+    }
+    return (lw >> 31) ^ sbit;
+}
+
 #ifndef METLDPC_CN_PAIR
 #define METLDPC_CN_PAIR 1   // two-lane path with packed fp32x2 ops (FADD2 / FFMA2)
 #endif
@@ -617,6 +657,12 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
 #endif
 #ifndef METLDPC_RING_CW2
 #define METLDPC_RING_CW2 19     // compute warps of the two-CNs-per-warp ring kernel (~100 registers)
+#endif
+#ifndef METLDPC_RING_CORE_HALF
+#define METLDPC_RING_CORE_HALF 0   // 1: core classes one 32-lane chunk per warp (cn_one), METLDPC_RING_CW_HALF warps
+#endif
+#ifndef METLDPC_RING_CW_HALF
+#define METLDPC_RING_CW_HALF 24
 #endif
 #ifndef METLDPC_RING_CW_CORE
 #define METLDPC_RING_CW_CORE 15 // compute warps of the ring kernel for classes with 5..16 active slots
@@ -868,10 +914,13 @@ struct RingCfg {
     // CNs per compute warp: 2 = one CN per half-warp, each thread four lanes (two fp32 pairs),
     // so the per-CN overhead is shared by two CNs (inner classes only)
     static constexpr int CPW = NA <= 4 ? METLDPC_RING_CPW : 1;
+    // core classes (NA > 4, no degree-1 slot): one 32-lane chunk per warp, two warps per CN
+    static constexpr bool HALF = NA > 4 && ND == 0 && METLDPC_RING_CORE_HALF;
     // compute warps = CNs per stage: 64 registers for the inner classes (NA <= 4), up to 128 for
     // the core classes (NA > 4, 16 warps per SM)
-    static constexpr int CW = NA <= 4 ? (CPW == 2 ? METLDPC_RING_CW2 : METLDPC_RING_CW) : METLDPC_RING_CW_CORE;
-    static constexpr int SC = CW * CPW;                               // CNs per stage
+    static constexpr int CW = NA <= 4 ? (CPW == 2 ? METLDPC_RING_CW2 : METLDPC_RING_CW)
+                                      : (HALF ? METLDPC_RING_CW_HALF : METLDPC_RING_CW_CORE);
+    static constexpr int SC = HALF ? CW / 2 : CW * CPW;               // CNs per stage
     static constexpr int RB = MSG ? 128 : 256;                        // r row bytes (64 lanes)
     // word arrays are copied from the 16-byte-aligned word at or below the first one needed
     // (lead 0..3 words) and rounded up to 16 bytes; the device arrays are padded for it
@@ -967,6 +1016,56 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
                 }
             }
         }
+    } else if constexpr (RC::HALF) {              // ---- compute warps, one 32-lane chunk each
+        const uint32_t tabk = phi_tab_lane<RULE>(smem, lane);
+        const uint32_t am0 = s_act[0], am1 = s_act[1];
+        const int c = warp & 1, cwn = warp >> 1;       // chunk, CN of the stage
+        const bool fr = (s_fresh[c] >> lane) & 1u;     // r^0 = 0 for a frame starting in this pass
+        uint32_t un = 0;
+        int slot = 0;
+        uint32_t phase = 0;
+        for (int gs = blockIdx.x; gs < nst; gs += gridDim.x) {
+            const int j0 = gs * SC, ncn = min(SC, count - j0);
+            mbar_wait(full_a + 8 * slot, phase);
+            if (cwn < ncn) {
+                const char* sp = ring + slot * RC::STG;
+                const int jl = j0 + cwn;
+                const int* sidx = reinterpret_cast<const int*>(sp + RC::OFF_IDX) + ((abase + j0 * NA) & 3) + cwn * NA;
+                const uint32_t* ssy = reinterpret_cast<const uint32_t*>(sp + RC::OFF_SY) + (((begin + j0) * 2) & 3) + cwn * 2;
+                const uint32_t sw = ssy[c];
+                const int lb = c * 32 + lane;               // the thread's lane in the group
+                uint32_t offs[NA];
+                float Lv[NA], ro[NA];
+#pragma unroll
+                for (int q = 0; q < NA; ++q) {
+                    offs[q] = uint32_t(sidx[q]) * 128u + uint32_t(lb);
+                    Lv[q] = __ldg(g.L + offs[q]);             // L2-resident gathers
+                }
+                const char* sr = sp + RC::OFF_R + cwn * NA * RC::RB;
+#pragma unroll
+                for (int q = 0; q < NA; ++q) {
+                    if constexpr (MSG) {   // half-word c of word `lane` (N7)
+                        const uint32_t w = reinterpret_cast<const unsigned short*>(sr)[q * 64 + 2 * lane + c];
+                        ro[q] = __fsub_rn(__uint_as_float(0x4B000000u | w), kMsg16Magic);
+                    } else {
+                        ro[q] = reinterpret_cast<const float*>(sr)[q * 64 + lb];
+                    }
+                    if (fr) ro[q] = 0.0f;
+                }
+                void* pr = MSG ? static_cast<void*>(reinterpret_cast<unsigned short*>(g.r) + size_t(abase + jl * NA) * 64 + 2 * lane + c)
+                               : static_cast<void*>(g.r + size_t(abase + jl * NA) * 64 + lb);
+                const uint32_t chk = cn_one<RULE, NA, MSG>(tabk, Lv, ro, (sw >> lane) & 1u, pr, g.L, offs);
+                un |= __ballot_sync(FULL, chk);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty_a + 8 * slot);
+            if (++slot == S) {
+                slot = 0;
+                phase ^= 1u;
+            }
+        }
+        const uint32_t am = c ? am1 : am0;
+        if (k.check && lane == 0 && (un & am)) atomicOr(&s_unsat[c], un & am);
     } else {                                       // ---- compute warps: CN(s) `warp` of every stage
         const uint32_t tabk = phi_tab_lane<RULE>(smem, lane);
         const uint32_t am0 = s_act[0], am1 = s_act[1];
