@@ -340,12 +340,11 @@ __device__ __forceinline__ uint32_t msg16_pack(float2 o) {
 // MSG = 0: r rows of fp32 (pr: float row pointer, ro: the messages).  MSG = 1: 16-bit rows
 // (pr: the thread's word of the row as uint32_t*, ro: the integers q of the stored messages,
 // x = fmaf(q, -2^-10, L) = the single rounding of L - q 2^-10, N7).
-// on = false (PRED only): compute but store nothing (the idle half-warp of a tail stage).
-template <int RULE, int NA, int ND, int MSG = 0, bool PRED = false>
+template <int RULE, int NA, int ND, int MSG = 0>
 __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 0 ? NA : 1],
                                          const float2 (&ro)[NA > 0 ? NA : 1], float2 lam, uint2 sbit, uint2 d1prev,
                                          void* prv, float* pla, const uint32_t (&offs)[NA > 0 ? NA : 1],
-                                         uint2& d1bit, bool on = true) {
+                                         uint2& d1bit) {
     float* pr = static_cast<float*>(prv);
     constexpr int D = NA + ND;
     const uint32_t one = one_bits();
@@ -393,7 +392,7 @@ __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 
         const float2 o = make_float2(
             __uint_as_float(__float_as_uint(fminf(ph.x, kRMax)) | ((par0 ^ xb0[s]) & 0x80000000u)),
             __uint_as_float(__float_as_uint(fminf(ph.y, kRMax)) | ((par1 ^ xb1[s]) & 0x80000000u)));
-        if (s < NA && (!PRED || on)) {
+        if (s < NA) {
             // Unpredicated: a latched or padding lane's r and accumulator columns are never
             // read for that lane again (k_finish keeps its L and clears the accumulator), and
             // full 256-byte rows avoid partial-sector writes.
@@ -413,46 +412,6 @@ __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 
         if (s > 0) Q = f2add(Q, p[s]);
     }
     return make_uint2((lw0 >> 31) ^ sbit.x ^ d1prev.x, (lw1 >> 31) ^ sbit.y ^ d1prev.y);
-}
-
-// DESIGN.md N1 for one CN and ONE lane, no degree-1 slot (the core classes of the half-warp ring
-// path): the element-wise operations of cn_pair in the same order.  MSG = 1: ro holds the integers q
-// of the 16-bit stored messages and prv the lane's half-word of the first r row.
-template <int RULE, int NA, int MSG>
-__device__ __forceinline__ uint32_t cn_one(uint32_t tabk, const float (&Lv)[NA], const float (&ro)[NA], uint32_t sbit,
-                                           void* prv, float* pla, const uint32_t (&offs)[NA]) {
-    const uint32_t one = one_bits();
-    float p[NA], P[NA];
-    uint32_t xb[NA];
-    uint32_t par = sbit << 31, lw = 0;
-#pragma unroll
-    for (int s = 0; s < NA; ++s) {
-        const float x = MSG ? __fmaf_rn(ro[s], -0.0009765625f, Lv[s]) : __fsub_rn(Lv[s], ro[s]);   // q = L - r (R10)
-        lw ^= __float_as_uint(Lv[s]);
-        xb[s] = __float_as_uint(x);
-        par ^= xb[s];
-        p[s] = phi_dev<RULE>(tabk, fabsf(x), one);
-    }
-    P[0] = 0.0f;
-    if constexpr (NA > 1) P[1] = p[0];
-#pragma unroll
-    for (int s = 2; s < NA; ++s) P[s] = __fadd_rn(P[s - 1], p[s - 1]);
-    float Q = 0.0f;
-#pragma unroll
-    for (int s = NA - 1; s >= 0; --s) {
-        const float S = (s == NA - 1) ? P[s] : (s == 0 ? Q : __fadd_rn(P[s], Q));
-        const float mag = fminf(phi_dev<RULE>(tabk, S, one), kRMax);
-        const float o = __uint_as_float(__float_as_uint(mag) | ((par ^ xb[s]) & 0x80000000u));
-        if constexpr (MSG) {
-            const uint32_t w = __float_as_uint(__fmaf_rn(o, 1024.0f, kMsg16Magic));   // stored message (N7)
-            __stcs(static_cast<unsigned short*>(prv) + s * 64, (unsigned short)(w & 0xFFFFu));
-        } else {
-            __stcs(static_cast<float*>(prv) + s * 64, o);
-        }
-        atomicAdd(reinterpret_cast<unsigned int*>(pla + offs[s] + 64), vn_fix(o));   // VN sum (Eq. 4, N3)
-        if (s > 0) Q = __fadd_rn(Q, p[s]);
-    }
-    return (lw >> 31) ^ sbit;
 }
 
 #ifndef METLDPC_CN_PAIR
@@ -655,23 +614,11 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
 #ifndef METLDPC_RING_CW
 #define METLDPC_RING_CW 23      // compute warps of the CN ring kernel (+ 1 producer warp; 80 registers)
 #endif
-#ifndef METLDPC_RING_CW2
-#define METLDPC_RING_CW2 19     // compute warps of the two-CNs-per-warp ring kernel (~100 registers)
-#endif
-#ifndef METLDPC_RING_CORE_HALF
-#define METLDPC_RING_CORE_HALF 0   // 1: core classes one 32-lane chunk per warp (cn_one), METLDPC_RING_CW_HALF warps
-#endif
-#ifndef METLDPC_RING_CW_HALF
-#define METLDPC_RING_CW_HALF 24
-#endif
 #ifndef METLDPC_RING_CW_CORE
 #define METLDPC_RING_CW_CORE 15 // compute warps of the ring kernel for classes with 5..16 active slots
 #endif
 #ifndef METLDPC_RING_STAGES
 #define METLDPC_RING_STAGES 6   // CTA ring depth cap (k_cn_ring)
-#endif
-#ifndef METLDPC_PIPE_LTMA
-#define METLDPC_PIPE_LTMA 0     // 1: the CN's posterior rows L_v also arrive by TMA into the ring stage
 #endif
 constexpr int kPipeStages = METLDPC_PIPE_STAGES;
 constexpr int kSmemPerSm = 232448;     // opt-in dynamic shared memory per block (227 KB)
@@ -679,9 +626,7 @@ constexpr int kSmemPerSm = 232448;     // opt-in dynamic shared memory per block
 template <int NA, int ND, int MSG = 0>
 struct PipeCfg {
     static constexpr int RB = MSG ? 128 : 256;                        // bytes per r row (64 lanes)
-    static constexpr bool LT = METLDPC_PIPE_LTMA != 0;                // L rows staged by TMA too
-    static constexpr int LOFF = NA * RB + ND * 256;                   // stage offset of the L rows
-    static constexpr int STG = LOFF + (LT ? NA * 256 : 0);            // bytes per stage: r, lambda[, L]
+    static constexpr int STG = NA * RB + ND * 256;                    // bytes per stage: r, lambda
     static constexpr int IDX = 32 * NA;                               // ints per staged tile
     static constexpr int WARP_BYTES = (2 * IDX * 4 + kPipeStages * STG + kPipeStages * 8 + 127) / 128 * 128;
     static constexpr int TAB = (PhiT<METLDPC_RULE_EXACT>::TAB_BYTES > PhiT<METLDPC_RULE_PHI_LUT>::TAB_BYTES)
@@ -715,12 +660,6 @@ __device__ __forceinline__ uint64_t l2_evict_first_policy() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
-}
-// Rows re-read every iteration (L): default L2 policy.
-__device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                 "l"(src), "r"(bytes), "r"(bar)
-                 : "memory");
 }
 // Streams read once per iteration (r, lambda): evict-first, so the L / accumulator rows stay in L2.
 __device__ __forceinline__ void tma_load_1d_ef(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
@@ -774,8 +713,8 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND, MSG>::THREADS, 1)
         const int jt = tile * TS, nt = min(TS, count - jt);
         for (int e = lane; e < nt * NA; e += 32) s_idx[b * PC::IDX + e] = __ldg(cd.a_vn + abase + jt * NA + e) * 128;
     };
-    // producer cursor (tile, index, index buffer) runs kPipeStages - 1 CNs ahead of the consumer
-    int pt = gw, pi = 0, pb = 0;
+    // producer cursor (tile, index) runs kPipeStages - 1 CNs ahead of the consumer
+    int pt = gw, pi = 0;
     uint32_t np = 0, nc = 0;
     auto produce = [&]() {
         if (pt >= ntiles) return;
@@ -786,14 +725,9 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND, MSG>::THREADS, 1)
             mbar_expect_tx(bar, PC::STG);
             tma_load_1d_ef(dst, reinterpret_cast<const char*>(g.r) + size_t(abase + jl * NA) * PC::RB, NA * PC::RB, bar, pol);
             if constexpr (ND > 0) tma_load_1d_ef(dst + NA * PC::RB, g.lam1 + size_t(dbase + jl) * 64, 256, bar, pol);
-            if constexpr (PC::LT) {   // posterior rows of the CN's active VNs (L2-resident; default policy)
-                const int* ib = s_idx + pb * PC::IDX + pi * NA;
-#pragma unroll
-                for (int s = 0; s < NA; ++s) tma_load_1d(dst + PC::LOFF + s * 256, g.L + ib[s], 256, bar);
-            }
         }
         ++np;
-        if (++pi == min(TS, count - pt * TS)) { pi = 0; pt += GW; pb ^= 1; }
+        if (++pi == min(TS, count - pt * TS)) { pi = 0; pt += GW; }
     };
     if (gw < ntiles) stage_idx(gw, 0);
     __syncwarp();
@@ -830,15 +764,10 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND, MSG>::THREADS, 1)
 #pragma unroll
             for (int s = 0; s < NA; ++s) {
                 offs[s] = uint32_t(idx[s]) + uint32_t(lane);
-                if constexpr (!PC::LT)
-                    L2[s] = make_float2(__ldg(g.L + offs[s]), __ldg(g.L + offs[s] + 32));   // L2-resident gathers
+                L2[s] = make_float2(__ldg(g.L + offs[s]), __ldg(g.L + offs[s] + 32));   // L2-resident gathers
             }
             mbar_wait(bar_a + 8 * st, ph);
             const float* sr = reinterpret_cast<const float*>(stage + st * PC::STG);
-            if constexpr (PC::LT) {
-#pragma unroll
-                for (int s = 0; s < NA; ++s) L2[s] = make_float2(sr[PC::LOFF / 4 + s * 64 + lane], sr[PC::LOFF / 4 + s * 64 + 32 + lane]);
-            }
 #pragma unroll
             for (int s = 0; s < NA; ++s) {
                 if constexpr (MSG) r2[s] = msg16_q(reinterpret_cast<const uint32_t*>(sr)[s * 32 + lane]);   // q (N7)
@@ -905,22 +834,13 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-#ifndef METLDPC_RING_CPW
-#define METLDPC_RING_CPW 1      // CNs per compute warp of the inner-class ring kernel (1, or 2 = one per half-warp)
-#endif
-
 template <int NA, int ND, int MSG>
 struct RingCfg {
-    // CNs per compute warp: 2 = one CN per half-warp, each thread four lanes (two fp32 pairs),
-    // so the per-CN overhead is shared by two CNs (inner classes only)
-    static constexpr int CPW = NA <= 4 ? METLDPC_RING_CPW : 1;
-    // core classes (NA > 4, no degree-1 slot): one 32-lane chunk per warp, two warps per CN
-    static constexpr bool HALF = NA > 4 && ND == 0 && METLDPC_RING_CORE_HALF;
+
     // compute warps = CNs per stage: 64 registers for the inner classes (NA <= 4), up to 128 for
     // the core classes (NA > 4, 16 warps per SM)
-    static constexpr int CW = NA <= 4 ? (CPW == 2 ? METLDPC_RING_CW2 : METLDPC_RING_CW)
-                                      : (HALF ? METLDPC_RING_CW_HALF : METLDPC_RING_CW_CORE);
-    static constexpr int SC = HALF ? CW / 2 : CW * CPW;               // CNs per stage
+    static constexpr int CW = NA <= 4 ? METLDPC_RING_CW : METLDPC_RING_CW_CORE;
+    static constexpr int SC = CW;                                     // CNs per stage
     static constexpr int RB = MSG ? 128 : 256;                        // r row bytes (64 lanes)
     // word arrays are copied from the 16-byte-aligned word at or below the first one needed
     // (lead 0..3 words) and rounded up to 16 bytes; the device arrays are padded for it
@@ -957,8 +877,7 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
     k_cn_ring(CodeDev cd, Group g, CnCtl karg, int begin, int count) {
     using PT = PhiT<RULE>;
     using RC = RingCfg<NA, ND, MSG>;
-    constexpr int CW = RC::CW, S = RC::STAGES, SC = RC::SC, CPW = RC::CPW;
-    constexpr int NP = CPW == 2 ? 2 : 1;           // lane pairs per thread
+    constexpr int CW = RC::CW, S = RC::STAGES, SC = RC::SC;
     extern __shared__ __align__(16) char smem[];
     __shared__ uint32_t s_unsat[2], s_act[2], s_fresh[2];
     pdl_launch_dependents();
@@ -1016,146 +935,66 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
                 }
             }
         }
-    } else if constexpr (RC::HALF) {              // ---- compute warps, one 32-lane chunk each
-        const uint32_t tabk = phi_tab_lane<RULE>(smem, lane);
-        const uint32_t am0 = s_act[0], am1 = s_act[1];
-        const int c = warp & 1, cwn = warp >> 1;       // chunk, CN of the stage
-        const bool fr = (s_fresh[c] >> lane) & 1u;     // r^0 = 0 for a frame starting in this pass
-        uint32_t un = 0;
-        int slot = 0;
-        uint32_t phase = 0;
-        for (int gs = blockIdx.x; gs < nst; gs += gridDim.x) {
-            const int j0 = gs * SC, ncn = min(SC, count - j0);
-            mbar_wait(full_a + 8 * slot, phase);
-            if (cwn < ncn) {
-                const char* sp = ring + slot * RC::STG;
-                const int jl = j0 + cwn;
-                const int* sidx = reinterpret_cast<const int*>(sp + RC::OFF_IDX) + ((abase + j0 * NA) & 3) + cwn * NA;
-                const uint32_t* ssy = reinterpret_cast<const uint32_t*>(sp + RC::OFF_SY) + (((begin + j0) * 2) & 3) + cwn * 2;
-                const uint32_t sw = ssy[c];
-                const int lb = c * 32 + lane;               // the thread's lane in the group
-                uint32_t offs[NA];
-                float Lv[NA], ro[NA];
-#pragma unroll
-                for (int q = 0; q < NA; ++q) {
-                    offs[q] = uint32_t(sidx[q]) * 128u + uint32_t(lb);
-                    Lv[q] = __ldg(g.L + offs[q]);             // L2-resident gathers
-                }
-                const char* sr = sp + RC::OFF_R + cwn * NA * RC::RB;
-#pragma unroll
-                for (int q = 0; q < NA; ++q) {
-                    if constexpr (MSG) {   // half-word c of word `lane` (N7)
-                        const uint32_t w = reinterpret_cast<const unsigned short*>(sr)[q * 64 + 2 * lane + c];
-                        ro[q] = __fsub_rn(__uint_as_float(0x4B000000u | w), kMsg16Magic);
-                    } else {
-                        ro[q] = reinterpret_cast<const float*>(sr)[q * 64 + lb];
-                    }
-                    if (fr) ro[q] = 0.0f;
-                }
-                void* pr = MSG ? static_cast<void*>(reinterpret_cast<unsigned short*>(g.r) + size_t(abase + jl * NA) * 64 + 2 * lane + c)
-                               : static_cast<void*>(g.r + size_t(abase + jl * NA) * 64 + lb);
-                const uint32_t chk = cn_one<RULE, NA, MSG>(tabk, Lv, ro, (sw >> lane) & 1u, pr, g.L, offs);
-                un |= __ballot_sync(FULL, chk);
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty_a + 8 * slot);
-            if (++slot == S) {
-                slot = 0;
-                phase ^= 1u;
-            }
-        }
-        const uint32_t am = c ? am1 : am0;
-        if (k.check && lane == 0 && (un & am)) atomicOr(&s_unsat[c], un & am);
-    } else {                                       // ---- compute warps: CN(s) `warp` of every stage
+    } else {                                       // ---- compute warps: CN `warp` of every stage
         const uint32_t tabk = phi_tab_lane<RULE>(smem, lane);
         const uint32_t am0 = s_act[0], am1 = s_act[1];
         const bool any_fresh = (s_fresh[0] | s_fresh[1]) != 0u;
-        // CPW = 1: the thread's lanes are (lane, lane + 32); CPW = 2: half-warp h takes CN 2 w + h,
-        // thread t = lane & 15 its lanes (t, t + 32) and (t + 16, t + 48)
-        const int sub = CPW == 2 ? (lane >> 4) : 0;
-        const int t0 = CPW == 2 ? (lane & 15) : lane;
-        uint32_t un0[NP], un1[NP];
-#pragma unroll
-        for (int q = 0; q < NP; ++q) un0[q] = un1[q] = 0u;
+        const bool f0 = (s_fresh[0] >> lane) & 1u, f1 = (s_fresh[1] >> lane) & 1u;
+        uint32_t un0 = 0, un1 = 0;
         int slot = 0;
         uint32_t phase = 0;   // parity of the slot's current use
         for (int gs = blockIdx.x; gs < nst; gs += gridDim.x) {
             const int j0 = gs * SC, ncn = min(SC, count - j0);
             mbar_wait(full_a + 8 * slot, phase);
-            if (warp * CPW < ncn) {
-                const int cw = warp * CPW + sub;          // CN of this (half-)warp within the stage
-                const bool on = CPW == 1 || cw < ncn;     // (CPW = 1: the warp test above)
-                const int cwc = (CPW == 1 || on) ? cw : cw - 1;   // an idle tail half reads its sibling's CN, stores nothing
+            if (warp < ncn) {
                 const char* sp = ring + slot * RC::STG;
-                const int jl = j0 + cwc;
-                const int* sidx = reinterpret_cast<const int*>(sp + RC::OFF_IDX) + ((abase + j0 * NA) & 3) + cwc * NA;
-                const uint32_t* ssy = reinterpret_cast<const uint32_t*>(sp + RC::OFF_SY) + (((begin + j0) * 2) & 3) + cwc * 2;
+                const int jl = j0 + warp;
+                const int* sidx = reinterpret_cast<const int*>(sp + RC::OFF_IDX) + ((abase + j0 * NA) & 3) + warp * NA;
+                uint32_t offs[NA];
+                float2 L2[NA], r2[NA];
+#pragma unroll
+                for (int s = 0; s < NA; ++s) {
+                    offs[s] = uint32_t(sidx[s]) * 128u + uint32_t(lane);
+                    L2[s] = make_float2(__ldg(g.L + offs[s]), __ldg(g.L + offs[s] + 32));   // L2-resident gathers
+                }
+                const uint32_t* ssy = reinterpret_cast<const uint32_t*>(sp + RC::OFF_SY) + (((begin + j0) * 2) & 3) + warp * 2;
                 const uint32_t swx = ssy[0], swy = ssy[1];
                 uint2 wv = make_uint2(0, 0);
                 if constexpr (ND > 0)
                     if (d1in) {
                         const uint32_t* sd =
-                            reinterpret_cast<const uint32_t*>(sp + RC::OFF_D1) + ((long(k.rpar) * cd.n_1 + dbase + j0) * 2 & 3) + cwc * 2;
+                            reinterpret_cast<const uint32_t*>(sp + RC::OFF_D1) + ((long(k.rpar) * cd.n_1 + dbase + j0) * 2 & 3) + warp * 2;
                         wv = make_uint2(sd[0], sd[1]);
                     }
-                const float* sr = reinterpret_cast<const float*>(sp + RC::OFF_R + cwc * NA * RC::RB);
-                const float* sl = reinterpret_cast<const float*>(sp + RC::OFF_L1 + cwc * 256);
-                uint32_t bx[NP], by[NP];   // ballots of the degree-1 decisions, per pair
+                const float* sr = reinterpret_cast<const float*>(sp + RC::OFF_R + warp * NA * RC::RB);
 #pragma unroll
-                for (int q = 0; q < NP; ++q) {
-                    const int base = t0 + 16 * q;         // the pair's first lane (second: base + 32)
-                    uint32_t offs[NA];
-                    float2 L2[NA], r2[NA];
-#pragma unroll
-                    for (int s = 0; s < NA; ++s) {
-                        offs[s] = uint32_t(sidx[s]) * 128u + uint32_t(base);
-                        L2[s] = make_float2(__ldg(g.L + offs[s]), __ldg(g.L + offs[s] + 32));   // L2-resident gathers
-                    }
+                for (int s = 0; s < NA; ++s) {
+                    if constexpr (MSG) r2[s] = msg16_q(reinterpret_cast<const uint32_t*>(sr)[s * 32 + lane]);
+                    else r2[s] = make_float2(sr[s * 64 + lane], sr[s * 64 + 32 + lane]);
+                }
+                if (any_fresh) {   // r^0 = 0 for a frame starting in this pass (Step 2), in registers
 #pragma unroll
                     for (int s = 0; s < NA; ++s) {
-                        if constexpr (MSG) r2[s] = msg16_q(reinterpret_cast<const uint32_t*>(sr)[s * 32 + base]);
-                        else r2[s] = make_float2(sr[s * 64 + base], sr[s * 64 + 32 + base]);
-                    }
-                    if (any_fresh) {   // r^0 = 0 for a frame starting in this pass (Step 2), in registers
-                        const bool f0 = (s_fresh[0] >> base) & 1u, f1 = (s_fresh[1] >> base) & 1u;
-#pragma unroll
-                        for (int s = 0; s < NA; ++s) {
-                            if (f0) r2[s].x = 0.0f;
-                            if (f1) r2[s].y = 0.0f;
-                        }
-                    }
-                    float2 lam = make_float2(0.0f, 0.0f);
-                    if constexpr (ND > 0) lam = make_float2(sl[base], sl[32 + base]);
-                    void* pr = MSG ? static_cast<void*>(reinterpret_cast<unsigned int*>(g.r) + (size_t(abase + jl * NA) * 32 + base))
-                                   : static_cast<void*>(g.r + (size_t(abase + jl * NA) * 64 + base));
-                    uint2 d1 = make_uint2(0, 0);
-                    const uint2 c2 = cn_pair<RULE, NA, ND, MSG, (CPW == 2)>(
-                        tabk, L2, r2, lam, make_uint2((swx >> base) & 1u, (swy >> base) & 1u),
-                        make_uint2((wv.x >> base) & 1u, (wv.y >> base) & 1u), pr, g.L, offs, d1, on);
-                    // syndrome-test flags of the lanes (CPW = 2: folded into 32-lane words at the end)
-                    un0[q] |= __ballot_sync(FULL, CPW == 1 ? c2.x : (c2.x && on));
-                    un1[q] |= __ballot_sync(FULL, CPW == 1 ? c2.y : (c2.y && on));
-                    if constexpr (ND > 0) {
-                        bx[q] = __ballot_sync(FULL, d1.x);
-                        by[q] = __ballot_sync(FULL, d1.y);
+                        if (f0) r2[s].x = 0.0f;
+                        if (f1) r2[s].y = 0.0f;
                     }
                 }
+                float2 lam = make_float2(0.0f, 0.0f);
                 if constexpr (ND > 0) {
-                    uint2 b;
-                    if constexpr (CPW == 2) {   // pair q of half h holds lanes 16 q + t of CN 2 w + h
-                        uint32_t x, y;
-                        if (sub == 0) {
-                            asm("prmt.b32 %0, %1, %2, 0x5410;" : "=r"(x) : "r"(bx[0]), "r"(bx[1]));
-                            asm("prmt.b32 %0, %1, %2, 0x5410;" : "=r"(y) : "r"(by[0]), "r"(by[1]));
-                        } else {
-                            asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(x) : "r"(bx[0]), "r"(bx[1]));
-                            asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(y) : "r"(by[0]), "r"(by[1]));
-                        }
-                        b = make_uint2(x, y);
-                    } else {
-                        b = make_uint2(bx[0], by[0]);
-                    }
-                    if (t0 == 0 && (CPW == 1 || on)) {
+                    const float* sl = reinterpret_cast<const float*>(sp + RC::OFF_L1 + warp * 256);
+                    lam = make_float2(sl[lane], sl[32 + lane]);
+                }
+                void* pr = MSG ? static_cast<void*>(reinterpret_cast<unsigned int*>(g.r) + (size_t(abase + jl * NA) * 32 + lane))
+                               : static_cast<void*>(g.r + (size_t(abase + jl * NA) * 64 + lane));
+                uint2 d1 = make_uint2(0, 0);
+                const uint2 c2 = cn_pair<RULE, NA, ND, MSG>(tabk, L2, r2, lam,
+                                                            make_uint2((swx >> lane) & 1u, (swy >> lane) & 1u),
+                                                            make_uint2((wv.x >> lane) & 1u, (wv.y >> lane) & 1u), pr, g.L, offs, d1);
+                un0 |= __ballot_sync(FULL, c2.x);
+                un1 |= __ballot_sync(FULL, c2.y);
+                if constexpr (ND > 0) {
+                    const uint2 b = make_uint2(__ballot_sync(FULL, d1.x), __ballot_sync(FULL, d1.y));
+                    if (lane == 0) {
                         uint2* wp = reinterpret_cast<uint2*>(g.d1bits) + (size_t(k.wpar) * cd.n_1 + dbase + jl);
                         if ((am0 & am1) != FULL) {
                             // keep the words of lanes not iterating, without a read on the warp's path:
@@ -1180,17 +1019,9 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
                 phase ^= 1u;
             }
         }
-        uint32_t u0, u1;
-        if constexpr (CPW == 2) {   // bit 16 h + t of pair q's ballot = lane 16 q + t of a CN
-            u0 = ((un0[0] | (un0[0] >> 16)) & 0xFFFFu) | ((un0[1] | (un0[1] << 16)) & 0xFFFF0000u);
-            u1 = ((un1[0] | (un1[0] >> 16)) & 0xFFFFu) | ((un1[1] | (un1[1] << 16)) & 0xFFFF0000u);
-        } else {
-            u0 = un0[0];
-            u1 = un1[0];
-        }
         if (k.check && lane == 0) {
-            if (u0 & am0) atomicOr(&s_unsat[0], u0 & am0);
-            if (u1 & am1) atomicOr(&s_unsat[1], u1 & am1);
+            if (un0 & am0) atomicOr(&s_unsat[0], un0 & am0);
+            if (un1 & am1) atomicOr(&s_unsat[1], un1 & am1);
         }
     }
     __syncthreads();
