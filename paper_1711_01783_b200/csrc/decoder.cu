@@ -398,9 +398,8 @@ metldpc_status group_loop(metldpc_decoder d, const GroupJob& j, int N) {
 
 // Lane-refill graph of workspace k ("refill ... from a frame queue", per lane):
 //   while (some lane iterates or waits) {
-//       CN classes; latch (per lane); finish;
-//       if (wave) { finalize finished lanes; assign next frames; scatter; syndrome; activate }
-//       pass counter++ }
+//       CN classes; latch (per lane, pass counter++, loop condition); finish;
+//       if (wave) { finalize finished lanes; assign next frames; scatter; syndrome; activate } }
 // The refill wave is an IF node, so passes without a wave cost nothing extra.
 metldpc_status stream_graph(metldpc_decoder d, int k, cudaGraphExec_t* out) {
     if (d->stream_exec[size_t(k)]) {
@@ -434,7 +433,7 @@ metldpc_status stream_graph(metldpc_decoder d, int k, cudaGraphExec_t* out) {
     cudaError_t e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
     if (e != cudaSuccess) return fail_capture(e, "stream graph capture: ");
     launch_cn_classes(d, cd, g, 0, true, cs, d->l2w[size_t(k)]);
-    launch_latch_stream(g, d->job, (unsigned long long)hi, cs, pdl_enabled());
+    launch_latch_stream(g, d->job, (unsigned long long)hi, (unsigned long long)hw, cs, pdl_enabled());
     launch_finish(cd, g, d->vn_grid, cs, d->l2w[size_t(k)], pdl_enabled());
     cudaGraph_t cap;
     if ((e = cudaStreamEndCapture(cs, &cap)) != cudaSuccess) return fail_capture(e, "stream graph capture: ");
@@ -461,11 +460,6 @@ metldpc_status stream_graph(metldpc_decoder d, int k, cudaGraphExec_t* out) {
     if ((e = cudaStreamBeginCaptureToGraph(cs, wave, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)) != cudaSuccess)
         return fail_capture(e, "stream graph capture: ");
     launch_refill_wave(cd, g, d->job, cs);
-    if ((e = cudaStreamEndCapture(cs, &cap)) != cudaSuccess) return fail_capture(e, "stream graph capture: ");
-    // part C: pass counter and loop condition, after the IF node
-    if ((e = cudaStreamBeginCaptureToGraph(cs, body, &inode, nullptr, 1, cudaStreamCaptureModeRelaxed)) != cudaSuccess)
-        return fail_capture(e, "stream graph capture: ");
-    launch_stream_ctl(g, d->job, (unsigned long long)hw, cs);
     if ((e = cudaStreamEndCapture(cs, &cap)) != cudaSuccess) return fail_capture(e, "stream graph capture: ");
     cudaStreamDestroy(cs);
     cudaGraphExec_t exec;
@@ -1299,7 +1293,7 @@ metldpc_status metldpc_get_profile(metldpc_decoder d, metldpc_profile_t* out) {
     *out = d->prof;
     if (d->stream_used) {   // streaming passes / waves are counted on the device
         CUDA_TRY(cudaDeviceSynchronize());
-        size_t per_pass = 3;   // latch, finish, loop control
+        size_t per_pass = 2;   // latch (+ loop control), finish
         for (const auto& c : d->cn_classes) per_pass += 1;
         for (const auto& w : d->ws) {
             uint32_t st[2] = {0, 0};

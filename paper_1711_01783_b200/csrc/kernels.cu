@@ -1465,7 +1465,13 @@ __global__ void k_stream_init(Group g) {
 // After CN pass l: per lane, latch a frame whose decisions of its iteration l_b - 1 satisfy
 // every check (ET), or whose final test (pass N + 1) is done; else count the iteration.
 // Requests a refill wave (IF node) once wave_min lanes wait or no lane iterates.
-__global__ void k_latch_stream(Group g, StreamJob* job, cudaGraphConditionalHandle if_h) {
+// Also the end of the pass: advances the global pass counter and sets the WHILE condition (loop
+// while any lane iterates or waits for its refill wave).  The condition is taken before the refill
+// wave of this pass; a wave that retires the last lanes costs one empty pass at the end of a decode.
+// (The pass cap only guards against a host-path queue that never fills: a correct run ends long
+// before it, when every frame has been decoded.)
+__global__ void k_latch_stream(Group g, StreamJob* job, cudaGraphConditionalHandle if_h,
+                               cudaGraphConditionalHandle while_h) {
     __shared__ uint32_t s_act[4], s_fin[4];
     pdl_launch_dependents();
     pdl_wait_previous();
@@ -1509,20 +1515,11 @@ __global__ void k_latch_stream(Group g, StreamJob* job, cudaGraphConditionalHand
             nfin += __popc(s_fin[q]);
         }
         cudaGraphSetConditional(if_h, (nfin > 0 && (nfin >= job->wave_min || nact == 0)) ? 1u : 0u);
+        *g.iter = l + 1;
+        const uint32_t passes = g.stat[0] + 1u;
+        g.stat[0] = passes;
+        cudaGraphSetConditional(while_h, ((nact + nfin) > 0 && passes < uint32_t(job->max_passes)) ? 1u : 0u);
     }
-}
-
-// End of a streaming pass: advance the global pass counter; loop while any lane iterates
-// or waits for its refill wave.
-// (The pass cap only guards against a host-path queue that never fills: a correct run ends
-// long before it, when every frame has been decoded.)
-__global__ void k_stream_ctl(Group g, const StreamJob* job, cudaGraphConditionalHandle while_h) {
-    *g.iter = *g.iter + 1;
-    const uint32_t passes = g.stat[0] + 1u;
-    g.stat[0] = passes;
-    uint32_t any = 0;
-    for (int q = 0; q < g.C; ++q) any |= g.act[q] | g.fin[q];
-    cudaGraphSetConditional(while_h, (any && passes < uint32_t(job->max_passes)) ? 1u : 0u);
 }
 
 // Refill wave 1/4: outputs of the finished lanes (as k_finalize, per lane: frame lane_frame,
@@ -2080,15 +2077,14 @@ void launch_latch_dev(const Group& g, bool et, cudaStream_t s, bool pdl) {
 
 void launch_stream_init(const Group& g, cudaStream_t s) { k_stream_init<<<1, 128, 0, s>>>(g); }
 
-void launch_latch_stream(const Group& g, StreamJob* job, unsigned long long if_handle, cudaStream_t s, bool pdl) {
+void launch_latch_stream(const Group& g, StreamJob* job, unsigned long long if_handle, unsigned long long while_handle,
+                         cudaStream_t s, bool pdl) {
     cudaGraphConditionalHandle h = cudaGraphConditionalHandle(if_handle);
-    void* args[] = {const_cast<Group*>(&g), &job, &h};
+    cudaGraphConditionalHandle hw = cudaGraphConditionalHandle(while_handle);
+    void* args[] = {const_cast<Group*>(&g), &job, &h, &hw};
     launch_small(reinterpret_cast<void*>(&k_latch_stream), dim3(1), dim3(128), args, s, pdl);
 }
 
-void launch_stream_ctl(const Group& g, const StreamJob* job, unsigned long long while_handle, cudaStream_t s) {
-    k_stream_ctl<<<1, 1, 0, s>>>(g, job, cudaGraphConditionalHandle(while_handle));
-}
 
 // Host path: frames [0, avail) of the queue are on the device (launched on the copy stream
 // after their H2D copies and LLR conversion, so stream order makes the data visible first).

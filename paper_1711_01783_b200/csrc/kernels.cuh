@@ -97,9 +97,9 @@ void launch_latch_dev(const Group& g, bool et, cudaStream_t s, bool pdl = false)
 void launch_loop_ctl(const Group& g, unsigned long long cond_handle, cudaStream_t s, bool pdl = false);
 // lane refill (streaming decode)
 void launch_stream_init(const Group& g, cudaStream_t s);
-void launch_latch_stream(const Group& g, StreamJob* job, unsigned long long if_handle, cudaStream_t s,
-                         bool pdl = false);
-void launch_stream_ctl(const Group& g, const StreamJob* job, unsigned long long while_handle, cudaStream_t s);
+// per-lane latch + end of a streaming pass (pass counter, WHILE condition), IF condition of the wave
+void launch_latch_stream(const Group& g, StreamJob* job, unsigned long long if_handle, unsigned long long while_handle,
+                         cudaStream_t s, bool pdl = false);
 void launch_refill_wave(const CodeDev& cd, const Group& g, StreamJob* job, cudaStream_t s);
 void launch_publish(StreamJob* job, int avail, cudaStream_t s);
 // l >= 1: iteration given by the host; l == 0: read from Group::iter (graph body), with

@@ -64,10 +64,9 @@ def main(out_path):
             dec = B.Decoder(h, F, max_iter=100, lane_refill=True)
             ms, prof, mi, cv = timed(dec, lam, sy)
             passes = prof["cn_launches"]
-            per_pass = (prof["launches"] - 5 * 0) // max(1, passes)
-            # launches = passes * (classes + 3) + waves * 5
+            # launches = passes * (classes + 2) + waves * 5 (since the loop control rides on the latch)
             ncls = 3
-            waves = (prof["launches"] - passes * (ncls + 3)) / 5
+            waves = (prof["launches"] - passes * (ncls + 2)) / 5
             rec = {"mode": "stream", "snr": snr, "wave_min": wmin, "ms": ms, "passes": passes, "waves": waves,
                    "mean_iters": mi, "converged": cv}
             rows.append((passes, waves, ms))
