@@ -617,9 +617,6 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
 #ifndef METLDPC_RING_CW_CORE
 #define METLDPC_RING_CW_CORE 15 // compute warps of the ring kernel for classes with 5..16 active slots
 #endif
-#ifndef METLDPC_RING_LSTAGE
-#define METLDPC_RING_LSTAGE 0   // 1: L rows of the stage's CNs staged in shared memory by the producer warp
-#endif
 #ifndef METLDPC_RING_STAGES
 #define METLDPC_RING_STAGES 6   // CTA ring depth cap (k_cn_ring)
 #endif
@@ -854,11 +851,7 @@ struct RingCfg {
     static constexpr int OFF_IDX = OFF_L1 + ND * SC * 256;
     static constexpr int OFF_SY = OFF_IDX + IDX_BYTES;
     static constexpr int OFF_D1 = OFF_SY + W_BYTES;
-    // METLDPC_RING_LSTAGE: the posterior rows L_v of the stage's CNs are staged too, by the producer
-    // warp's cp.async (32 lanes, 16 bytes each; completion counted on the full barrier)
-    static constexpr bool LST = METLDPC_RING_LSTAGE && NA <= 4;
-    static constexpr int OFF_LR = (OFF_D1 + ND * W_BYTES + 15) / 16 * 16;
-    static constexpr int STG = OFF_LR + (LST ? SC * NA * 256 : 0);
+    static constexpr int STG = OFF_D1 + ND * W_BYTES;
     static constexpr int TAB = (PhiT<METLDPC_RULE_EXACT>::TAB_BYTES > PhiT<METLDPC_RULE_PHI_LUT>::TAB_BYTES)
                                    ? PhiT<METLDPC_RULE_EXACT>::TAB_BYTES
                                    : PhiT<METLDPC_RULE_PHI_LUT>::TAB_BYTES;
@@ -904,7 +897,7 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
     }
     if (threadIdx.x == 32 * CW) {
         for (int st = 0; st < S; ++st) {
-            mbar_init(full_a + 8 * st, RC::LST ? 33 : 1);   // + the producer lanes' cp.async arrivals
+            mbar_init(full_a + 8 * st, 1);
             mbar_init(empty_a + 8 * st, CW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -916,30 +909,11 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
     load_phi_table<RULE>(smem, cd.phi);
     __syncthreads();
     if (warp == CW) {                              // ---- producer warp
-        if (RC::LST || lane == 0) {
+        if (lane == 0) {
             const uint64_t pol = l2_evict_first_policy();
             int slot = 0, use = 0;
             for (int gs = blockIdx.x; gs < nst; gs += gridDim.x) {
                 if (use) mbar_wait(empty_a + 8 * slot, (use - 1) & 1);
-                if constexpr (RC::LST) {   // L rows of the stage: 16 lanes per 256-byte row, two rows per step
-                    const int j0l = gs * SC, nrow = min(SC, count - j0l) * NA;
-                    const uint32_t ldst = ring_a + slot * RC::STG + RC::OFF_LR;
-                    for (int e = lane >> 4; e < nrow; e += 2) {
-                        const int a = __ldg(cd.a_vn + abase + j0l * NA + e);
-                        const char* src = reinterpret_cast<const char*>(g.L + size_t(a) * 128) + (lane & 15) * 16;
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ldst + e * 256 + (lane & 15) * 16),
-                                     "l"(src)
-                                     : "memory");
-                    }
-                    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full_a + 8 * slot) : "memory");
-                    if (lane != 0) {
-                        if (++slot == S) {
-                            slot = 0;
-                            ++use;
-                        }
-                        continue;
-                    }
-                }
                 const int j0 = gs * SC, ncn = min(SC, count - j0);
                 const uint32_t dst = ring_a + slot * RC::STG, bar = full_a + 8 * slot;
                 const long wi = long(abase) + long(j0) * NA, ws = (long(begin) + j0) * 2,
@@ -981,12 +955,7 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
 #pragma unroll
                 for (int s = 0; s < NA; ++s) {
                     offs[s] = uint32_t(sidx[s]) * 128u + uint32_t(lane);
-                    if constexpr (RC::LST) {
-                        const float* sl = reinterpret_cast<const float*>(sp + RC::OFF_LR) + (warp * NA + s) * 64;
-                        L2[s] = make_float2(sl[lane], sl[lane + 32]);
-                    } else {
-                        L2[s] = make_float2(__ldg(g.L + offs[s]), __ldg(g.L + offs[s] + 32));   // L2-resident gathers
-                    }
+                    L2[s] = make_float2(__ldg(g.L + offs[s]), __ldg(g.L + offs[s] + 32));   // L2-resident gathers
                 }
                 const uint32_t* ssy = reinterpret_cast<const uint32_t*>(sp + RC::OFF_SY) + (((begin + j0) * 2) & 3) + warp * 2;
                 const uint32_t swx = ssy[0], swy = ssy[1];

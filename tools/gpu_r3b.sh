@@ -1,0 +1,20 @@
+#!/bin/bash
+# GPU call: A/B of the L rows staged by the producer warp (index loads one stage ahead), 23/19/15 compute warps; ncu of base and variant
+set -x
+O=gpurun_out/r3b; mkdir -p $O
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
+V=$PWD/scratch/variants
+B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-et --frames 256"
+for rep in 1 2; do
+  for m in 32 16; do
+    timeout 300 $B --msg-bits $m > $O/ab_base_m${m}_$rep.json 2>>$O/ab.err
+    for v in lst lst19 lst15; do
+      METLDPC_LIB=$V/$v/libmetldpc.so timeout 300 $B --msg-bits $m > $O/ab_${v}_m${m}_$rep.json 2>>$O/ab.err
+    done
+  done
+done
+N="ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k regex:k_cn_ring<0,.3 --launch-skip 1 -c 1"
+R="python bench.py --steps 1 --warmup 0 --frames 64 --iters 8 --no-et --no-cpu-baseline --no-e2e"
+timeout 600 $N -o $O/ring_base $R > $O/ncu_base.log 2>&1
+METLDPC_LIB=$V/lst/libmetldpc.so timeout 600 $N -o $O/ring_lst $R > $O/ncu_lst.log 2>&1
+METLDPC_LIB=$V/lst/libmetldpc.so timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_msg16.py -x -q -k "c1 or msg16 or refill" > $O/pytest_lst.log 2>&1; echo "rc=$?" >> $O/pytest_lst.log
