@@ -493,10 +493,11 @@ metldpc_status stream_setup(metldpc_decoder d, int32_t batch, const float* llr, 
     h.N = N;
     h.avail = avail;
     {
-        // refill once 8 lanes have finished (measured at the headline config, r0.1de BIAWGN 0.161,
-        // 1024 frames: 4 / 8 / 16 / 32 -> 1579 / 1583 / 1446 / 1441 Mb/s)
+        // refill once 2 lanes have finished (headline config, r0.1de BIAWGN 0.161, 4096 frames per
+        // call, same box: thresholds 1 / 2 / 4 / 8 -> 1855 / 1856 / 1844 / 1809 Mb/s with the
+        // lane-list wave kernels; 8 was best while a wave cost 0.17 ms, profiles/r2_wave_parts.jsonl)
         const char* e = std::getenv("METLDPC_REFILL_MIN");
-        h.wave_min = (e && std::atoi(e) > 0) ? std::atoi(e) : 8;
+        h.wave_min = (e && std::atoi(e) > 0) ? std::atoi(e) : 2;
     }
     // hang guard only: a lane needs at most N + 1 passes per frame
     const int64_t guard = (int64_t(batch) + d->B) * (int64_t(N) + 2) + 1000;

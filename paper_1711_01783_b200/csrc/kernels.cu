@@ -1524,43 +1524,79 @@ __global__ void k_latch_stream(Group g, StreamJob* job, cudaGraphConditionalHand
 
 // Refill wave 1/4: outputs of the finished lanes (as k_finalize, per lane: frame lane_frame,
 // degree-1 decisions from buffer lane_fbuf).
+// Lanes of a chunk set in `mask` (and, if need_frame, holding a frame), listed in shared memory
+// in lane order by the first C warps of the block (lane index, frame); returns the count.
+__device__ __forceinline__ int list_lanes(const Group& g, const uint32_t* mask, bool need_frame, int* s_b, int* s_f,
+                                          int* s_cnt) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int f = -1;
+    bool in = false;
+    uint32_t bal = 0;
+    if (w < g.C) {
+        const int b = w * 32 + lane;
+        in = (mask[w] >> lane) & 1u;
+        if (in) f = g.lane_frame[b];
+        if (need_frame) in = in && f >= 0;
+        bal = __ballot_sync(FULL, in);
+        if (lane == 0) s_cnt[w] = __popc(bal);
+    }
+    __syncthreads();
+    if (w < g.C && in) {
+        int pos = __popc(bal & ((1u << lane) - 1u));   // rank in the chunk
+        for (int q = 0; q < w; ++q) pos += s_cnt[q];
+        s_b[pos] = w * 32 + lane;
+        s_f[pos] = f;
+    }
+    __syncthreads();
+    int tot = 0;
+    for (int q = 0; q < g.C; ++q) tot += s_cnt[q];
+    return tot;
+}
+
+// Refill wave 1/4: hard bits (original VN order, packed) of the lanes whose frame finished.  A warp
+// owns one word of 32 VNs (thread = VN, one coalesced index load) and serves every finished lane
+// of the group from it: per lane one load per thread (the VN's L entry or degree-1 decision word,
+// the lane's column) and one ballot -- four lanes' loads in flight at a time.
 __global__ void __launch_bounds__(256) k_finalize_lanes(CodeDev cd, Group g, StreamJob* job) {
+    __shared__ int s_b[128], s_f[128], s_cnt[4];
     const int NW = (cd.n + 31) >> 5;
+    const int nfin = list_lanes(g, g.fin, true, s_b, s_f, s_cnt);
+    if (nfin == 0) return;
     const int lane = threadIdx.x & 31;
+    if (blockIdx.x == 0)
+        for (int q = threadIdx.x; q < nfin; q += blockDim.x) {
+            job->iters[s_f[q]] = g.iters[s_b[q]];
+            job->conv[s_f[q]] = g.conv[s_b[q]];
+        }
     const int wblk = blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int c = blockIdx.y;
-    const int b = c * 32 + lane;
-    const bool mine = (g.fin[c] >> lane) & 1u;
-    const int f = mine ? g.lane_frame[b] : -1;
-    if (__ballot_sync(FULL, f >= 0) == 0u || wblk >= NW) {   // warp-uniform exits
-        if (f >= 0 && blockIdx.x == 0 && threadIdx.x < 32) {
-            job->iters[f] = g.iters[b];
-            job->conv[f] = g.conv[b];
-        }
-        return;
-    }
-    const int it = f >= 0 ? g.iters[b] : 0;
-    if (f >= 0 && blockIdx.x == 0 && threadIdx.x < 32) {
-        job->iters[f] = it;
-        job->conv[f] = g.conv[b];
-    }
-    const size_t off = size_t(c) * 32 + lane;
-    const int par = f >= 0 ? g.lane_fbuf[b] : 0;
-    const int i0 = wblk * 32;
-    // the word's 32 VN indices in one coalesced load, then 32 independent loads in flight
-    const int vm = (i0 + lane < cd.n) ? __ldg(cd.vmap + i0 + lane) : 0;
-    uint32_t word = 0;
+    if (wblk >= NW) return;
+    const int i = wblk * 32 + lane;
+    const int v = (i < cd.n) ? __ldg(cd.vmap + i) : 0;
+    const bool act = v >= 0 && i < cd.n, d1 = v < 0 && i < cd.n;
+    const float* Lv = g.L + size_t(act ? v : 0) * 2 * g.B;
+    const size_t d1off = size_t(d1 ? ~v : 0) * g.C;
+    for (int q0 = 0; q0 < nfin; q0 += 4) {
+        uint32_t bits[4];
 #pragma unroll
-    for (int ii = 0; ii < 32; ++ii) {
-        const int v = __shfl_sync(FULL, vm, ii);
-        uint32_t bit = 0;
-        if (f >= 0 && i0 + ii < cd.n) {
-            if (v >= 0) bit = g.L[size_t(v) * 2 * g.B + off] < 0.0f;
-            else bit = (g.d1bits[(size_t(par) * cd.n_1 + ~v) * g.C + c] >> lane) & 1u;
+        for (int u = 0; u < 4; ++u) {
+            const int q = min(q0 + u, nfin - 1);
+            const int b = s_b[q], c = b >> 5;
+            const int par = g.lane_fbuf[b];
+            uint32_t bit = 0;
+            if (act) bit = Lv[b] < 0.0f;
+            else if (d1) bit = (g.d1bits[size_t(par) * cd.n_1 * g.C + d1off + c] >> (b & 31)) & 1u;
+            bits[u] = bit;
         }
-        word |= bit << ii;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t word = __ballot_sync(FULL, bits[u]);
+            const int q = q0 + u;
+            if (q < nfin && lane == u) {
+                const int b = s_b[q];
+                job->bits[size_t(s_f[q]) * NW + wblk] = (g.iters[b] < 0) ? 0u : word;
+            }
+        }
     }
-    if (f >= 0) job->bits[size_t(f) * NW + wblk] = (it < 0) ? 0u : word;
 }
 
 // Refill wave 2/4: the finished lanes take the next frames of the queue (in lane order),
@@ -1615,53 +1651,45 @@ __global__ void k_refill_assign(Group g, StreamJob* job) {
 }
 
 // Refill wave 3/4: lambda of the new frames into their lanes' columns (lam_a, L = lambda,
-// accumulator 0, lam1), and their S_B bits into synd_t -- the k_scatter / k_pack_syndrome
-// transposes restricted to the new lanes.
+// accumulator 0, lam1).  Work item = (new lane, 32 consecutive VNs): one coalesced load of the
+// frame's LLRs and of the VN indices, then one store per thread into the VN's row; four items'
+// loads in flight per warp.  (The S_B bits follow in k_refill_synd.)
 __global__ void __launch_bounds__(256) k_refill_scatter(CodeDev cd, Group g, StreamJob* job) {
-    __shared__ float tile[32][33];
-    const int c = blockIdx.y;
-    const uint32_t nm = g.newm[c];
-    if (!nm) return;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const size_t off = size_t(c) * 32 + lane;
-    const bool mine = (nm >> lane) & 1u;
-    // frames of the new lanes (warp w reads rows w, w + 8, ...; rows of other lanes stay 0)
-    int fr[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int rr = w + 8 * q;
-        fr[q] = ((nm >> rr) & 1u) ? g.lane_frame[c * 32 + rr] : -1;
-    }
+    __shared__ int s_b[128], s_f[128], s_cnt[4];
+    const int nnew = list_lanes(g, g.newm, false, s_b, s_f, s_cnt);
+    if (nnew == 0) return;
+    const int lane = threadIdx.x & 31;
     const int ntiles = (cd.n + 31) / 32;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {   // a few tiles of 32 VNs per block
-        const int i0 = t * 32;
+    const long total = long(nnew) * ntiles;
+    const long GW = long(gridDim.x) * (blockDim.x >> 5);
+    for (long t0 = long(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); t0 < total; t0 += 4 * GW) {
+        float val[4];
+        int vm[4], bb[4], ii[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int i = i0 + lane;
-            tile[w + 8 * q][lane] = (fr[q] >= 0 && i < cd.n) ? __ldcv(job->llr + size_t(fr[q]) * cd.n + i) : 0.0f;
+        for (int u = 0; u < 4; ++u) {
+            const long t = t0 + u * GW;
+            const int q = t < total ? int(t / ntiles) : 0;
+            const int i = t < total ? int(t - long(q) * ntiles) * 32 + lane : cd.n;
+            bb[u] = s_b[q];
+            ii[u] = i;
+            val[u] = (i < cd.n) ? __ldcv(job->llr + size_t(s_f[q]) * cd.n + i) : 0.0f;
+            vm[u] = (i < cd.n) ? __ldg(cd.vmap + i) : 0;
         }
-        // the tile's VN indices: one coalesced load, broadcast by shuffles
-        const int vm = (i0 + lane < cd.n) ? __ldg(cd.vmap + i0 + lane) : 0;
-        __syncthreads();
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int ii = w + 8 * q, i = i0 + ii;
-            const int v = __shfl_sync(FULL, vm, ii);
-            if (i >= cd.n) break;
-            const float val = tile[lane][ii];
-            const uint32_t bad = __ballot_sync(FULL, mine && !isfinite(val));
-            if (bad && lane == 0) atomicOr(g.invalid + c, bad);
-            if (!mine) continue;
+        for (int u = 0; u < 4; ++u) {
+            const int b = bb[u];
+            if (__ballot_sync(FULL, ii[u] < cd.n && !isfinite(val[u])) && lane == 0) atomicOr(g.invalid + (b >> 5), 1u << (b & 31));
+            if (ii[u] >= cd.n) continue;
+            const int v = vm[u];
             if (v >= 0) {
-                const float lz = __fadd_rn(val, 0.0f);      // -0 -> +0, as k_scatter
-                g.lam_a[size_t(v) * g.B + off] = lz;
-                g.L[size_t(v) * 2 * g.B + off] = lz;
-                g.L[size_t(v) * 2 * g.B + g.B + off] = 0.0f;
+                const float lz = __fadd_rn(val[u], 0.0f);   // -0 -> +0, as k_scatter
+                g.lam_a[size_t(v) * g.B + b] = lz;
+                g.L[size_t(v) * 2 * g.B + b] = lz;
+                g.L[size_t(v) * 2 * g.B + g.B + b] = 0.0f;
             } else {
-                g.lam1[size_t(~v) * g.B + off] = lam1_phi_form(cd, val);
+                g.lam1[size_t(~v) * g.B + b] = lam1_phi_form(cd, val[u]);
             }
         }
-        __syncthreads();
     }
 }
 
@@ -2097,9 +2125,9 @@ void launch_publish(StreamJob* job, int avail, cudaStream_t s) { k_publish<<<1, 
 
 void launch_refill_wave(const CodeDev& cd, const Group& g, StreamJob* job, cudaStream_t s) {
     const int NW = (cd.n + 31) / 32, W = (cd.m + 31) / 32;
-    k_finalize_lanes<<<dim3((NW + 7) / 8, g.C), 256, 0, s>>>(cd, g, job);
+    k_finalize_lanes<<<unsigned((NW + 7) / 8), 256, 0, s>>>(cd, g, job);
     k_refill_assign<<<1, 128, 0, s>>>(g, job);
-    k_refill_scatter<<<dim3(std::min((cd.n + 31) / 32, 148 * 8), g.C), 256, 0, s>>>(cd, g, job);
+    k_refill_scatter<<<148 * 8, 256, 0, s>>>(cd, g, job);
     k_refill_synd<<<unsigned((long(W) * g.C + 7) / 8), 256, 0, s>>>(cd, g, job);
     k_refill_activate<<<1, 128, 0, s>>>(g);
 }
