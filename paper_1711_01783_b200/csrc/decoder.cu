@@ -697,7 +697,7 @@ metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, cons
     d->ws.resize(size_t(d->K));
     for (auto& w : d->ws) {
         if ((s = dalloc(&w.r, size_t(L.E_it) * B * size_t(cfg.msg_bits) / 32)) || (s = dalloc(&w.L, 2 * size_t(L.n_a) * B)) ||
-            (s = dalloc(&w.lam_a, size_t(L.n_a) * B)) || (s = dalloc(&w.lam1, size_t(L.n_1) * B)) ||
+            (s = dalloc(&w.lam_a, size_t(L.n_a) * B)) || (s = dalloc(&w.lam1, size_t((L.n_1 + 15) & ~7) * B)) ||
             (s = dalloc(&w.d1bits, 2 * size_t(L.n_1) * C + 8)) || (s = dalloc(&w.synd_t, size_t(L.m) * C + 8)) ||
             (s = dalloc(&w.ctl, 32)) || (s = dalloc(&w.iters, B)) || (s = dalloc(&w.conv, B)) ||
             (s = dalloc(&w.lane_l, B)) || (s = dalloc(&w.lane_frame, B)) || (s = dalloc(&w.lane_fbuf, B)) ||

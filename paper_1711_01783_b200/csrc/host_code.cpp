@@ -118,6 +118,23 @@ metldpc_status build_layout(int32_t n, int32_t m, int64_t E, const int64_t* cn_p
     };
     std::vector<std::vector<int32_t>> buckets(generic_key + 1);
     for (int32_t j = 0; j < m; ++j) buckets[cls_key(j)].push_back(j);
+    // An exact class with one degree-1 slot lists its CNs by the original index of that degree-1
+    // VN, so consecutive degree-1 slots q hold VNs in ascending original order: a frame's priors
+    // then land in whole 32-byte sectors of the blocked lam1 layout.
+    for (int key = 1; key < generic_key; key += 2) {
+        auto& bk = buckets[key];
+        if (bk.size() < 2) continue;
+        std::vector<std::pair<int32_t, int32_t>> kv;
+        kv.reserve(bk.size());
+        for (int32_t j : bk) {
+            int32_t v1 = -1;
+            for (int64_t e = cn_ptr[j]; e < cn_ptr[j + 1]; ++e)
+                if (deg[edge_vn[e]] < min_act) v1 = edge_vn[e];
+            kv.emplace_back(v1, j);
+        }
+        std::stable_sort(kv.begin(), kv.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        for (size_t i = 0; i < bk.size(); ++i) bk[i] = kv[i].second;
+    }
     std::vector<int32_t> order;
     order.reserve(m);
     for (int key = 0; key <= generic_key; ++key) {
@@ -136,6 +153,7 @@ metldpc_status build_layout(int32_t n, int32_t m, int64_t E, const int64_t* cn_p
     int32_t t = 0, n_1 = 0;
     for (int32_t jn = 0; jn < m; ++jn) {
         const int32_t j = order[jn];
+
         L.cn_aptr[jn] = t;
         L.cn_dptr[jn] = n_1;
         L.max_cn_deg = std::max(L.max_cn_deg, int32_t(cn_ptr[j + 1] - cn_ptr[j]));

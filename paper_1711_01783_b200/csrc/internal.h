@@ -34,11 +34,13 @@ metldpc_status fail(metldpc_status s, const std::string& msg);
 // Host layout of H (DESIGN.md section 6 "Data layout").
 //   CN label        j' in [0, m): CNs relabelled so every degree class is one contiguous
 //                   range (classes by total degree D = 0..16, then one class for 17..32),
-//                   ascending original index within a class
+//                   ascending original index within a class (classes with one degree-1
+//                   slot: ascending original index of the degree-1 VN)
 //   active VN index a in [0, n_a): VNs of degree >= 2, ascending original index
 //   active edge id  t in [0, E_it): edges of active VNs, CN-major in j' order, CSR order
 //                   within a row (perm_r maps t to the canonical active-edge CSR order)
-//   degree-1 slot   q in [0, n_1): edges of degree-1 VNs, same order
+//   degree-1 slot   q in [0, n_1): edges of degree-1 VNs, same order (so a class with one
+//                   degree-1 slot has them in ascending original VN order)
 struct HostLayout {
     int32_t n = 0, m = 0;
     int64_t E = 0, E_it = 0;

@@ -124,6 +124,15 @@ __device__ __forceinline__ float phi_gmem_rule(const float* tab, float y) {
     }
 }
 
+// lam1 layout: [n_1 / 8][B lanes][8].  Lane b's priors of 8 consecutive
+// degree-1 slots fill one 32-byte sector, so a frame's priors are written in whole sectors (the
+// refill wave writes one lane at a time); a ring stage of 24 consecutive checks is 3 contiguous
+// blocks (one bulk copy).  The slot inside the sector is XOR-swizzled by lane, so the 32 lanes
+// of a warp reading one slot hit 32 distinct shared-memory banks.
+__host__ __device__ __forceinline__ size_t lam1_idx(int q, int b, int B) {
+    return size_t(q >> 3) * size_t(8 * B) + size_t(b) * 8 + size_t((q & 7) ^ ((b >> 2) & 7));
+}
+
 // Degree-1 prior as the CN kernels read it (N1): phi(|lambda|) with the sign bit
 // [lambda < 0] (an input of -0 carries no sign, R2).
 __device__ __forceinline__ float lam1_phi_form(const CodeDev& cd, float lam) {
@@ -523,9 +532,8 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
                 }
                 uint2 wv = make_uint2(0, 0);
                 if constexpr (ND > 0) {
-                    const float* pl = g.lam1 + (size_t(q0) * 64 + c0 * 32 + lane);
 #pragma unroll
-                    for (int h = 0; h < LPT; ++h) lam[h] = __ldcs(pl + h * 32);
+                    for (int h = 0; h < LPT; ++h) lam[h] = __ldcs(g.lam1 + lam1_idx(q0, (c0 + h) * 32 + lane, 64));
                     if (k.check) wv = __ldg(reinterpret_cast<const uint2*>(g.d1bits) + (size_t(k.rpar) * cd.n_1 + q0));
                 } else {
 #pragma unroll
@@ -612,7 +620,7 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
 #define METLDPC_PIPE_WARPS 32   // warps per CTA cap (at most what the rings leave room for)
 #endif
 #ifndef METLDPC_RING_CW
-#define METLDPC_RING_CW 23      // compute warps of the CN ring kernel (+ 1 producer warp; 80 registers)
+#define METLDPC_RING_CW 24      // compute warps of the CN ring kernel (+ 1 producer warp; a multiple of 8)
 #endif
 #ifndef METLDPC_RING_CW_CORE
 #define METLDPC_RING_CW_CORE 15 // compute warps of the ring kernel for classes with 5..16 active slots
@@ -626,7 +634,7 @@ constexpr int kSmemPerSm = 232448;     // opt-in dynamic shared memory per block
 template <int NA, int ND, int MSG = 0>
 struct PipeCfg {
     static constexpr int RB = MSG ? 128 : 256;                        // bytes per r row (64 lanes)
-    static constexpr int STG = NA * RB + ND * 256;                    // bytes per stage: r, lambda
+    static constexpr int STG = NA * RB;                               // bytes per stage: r rows
     static constexpr int IDX = 32 * NA;                               // ints per staged tile
     static constexpr int WARP_BYTES = (2 * IDX * 4 + kPipeStages * STG + kPipeStages * 8 + 127) / 128 * 128;
     static constexpr int TAB = (PhiT<METLDPC_RULE_EXACT>::TAB_BYTES > PhiT<METLDPC_RULE_PHI_LUT>::TAB_BYTES)
@@ -724,7 +732,6 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND, MSG>::THREADS, 1)
             const uint32_t bar = bar_a + 8 * st, dst = stage_a + st * PC::STG;
             mbar_expect_tx(bar, PC::STG);
             tma_load_1d_ef(dst, reinterpret_cast<const char*>(g.r) + size_t(abase + jl * NA) * PC::RB, NA * PC::RB, bar, pol);
-            if constexpr (ND > 0) tma_load_1d_ef(dst + NA * PC::RB, g.lam1 + size_t(dbase + jl) * 64, 256, bar, pol);
         }
         ++np;
         if (++pi == min(TS, count - pt * TS)) { pi = 0; pt += GW; }
@@ -784,7 +791,8 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND, MSG>::THREADS, 1)
                 }
             }
             float2 lam = make_float2(0.0f, 0.0f);
-            if constexpr (ND > 0) lam = make_float2(sr[NA * PC::RB / 4 + lane], sr[NA * PC::RB / 4 + 32 + lane]);
+            if constexpr (ND > 0)   // blocked lam1 rows: two direct loads (this kernel is the METLDPC_RING=0 path)
+                lam = make_float2(__ldcs(g.lam1 + lam1_idx(dbase + jl, lane, 64)), __ldcs(g.lam1 + lam1_idx(dbase + jl, lane + 32, 64)));
             void* pr = MSG ? static_cast<void*>(reinterpret_cast<unsigned int*>(g.r) + (size_t(abase + jl * NA) * 32 + lane))
                            : static_cast<void*>(g.r + (size_t(abase + jl * NA) * 64 + lane));
             uint2 d1 = make_uint2(0, 0);
@@ -841,6 +849,7 @@ struct RingCfg {
     // the core classes (NA > 4, 16 warps per SM)
     static constexpr int CW = NA <= 4 ? METLDPC_RING_CW : METLDPC_RING_CW_CORE;
     static constexpr int SC = CW;                                     // CNs per stage
+    static_assert(ND == 0 || SC % 8 == 0, "a stage's lam1 rows must be whole blocks of 8 slots");
     static constexpr int RB = MSG ? 128 : 256;                        // r row bytes (64 lanes)
     // word arrays are copied from the 16-byte-aligned word at or below the first one needed
     // (lead 0..3 words) and rounded up to 16 bytes; the device arrays are padded for it
@@ -904,7 +913,11 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
     }
     const int abase = __ldg(cd.cn_aptr + begin);
     const int dbase = ND ? __ldg(cd.cn_dptr + begin) : 0;
-    const int nst = (count + SC - 1) / SC;
+    // Stages are aligned to the lam1 blocks: stage gs covers class positions [gs SC - lo, (gs + 1) SC - lo),
+    // lo = dbase mod 8, so every stage's degree-1 slots are whole 8-slot blocks (the first stage is
+    // lo checks short).  Without degree-1 slots lo = 0.
+    const int lo = ND ? (dbase & 7) : 0;
+    const int nst = (count + lo + SC - 1) / SC;
     const bool d1in = ND > 0 && k.check;           // degree-1 decisions of l - 1 for the syndrome test
     load_phi_table<RULE>(smem, cd.phi);
     __syncthreads();
@@ -914,17 +927,19 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
             int slot = 0, use = 0;
             for (int gs = blockIdx.x; gs < nst; gs += gridDim.x) {
                 if (use) mbar_wait(empty_a + 8 * slot, (use - 1) & 1);
-                const int j0 = gs * SC, ncn = min(SC, count - j0);
+                const int j0 = max(gs * SC - lo, 0), ncn = min((gs + 1) * SC - lo, count) - j0;
                 const uint32_t dst = ring_a + slot * RC::STG, bar = full_a + 8 * slot;
                 const long wi = long(abase) + long(j0) * NA, ws = (long(begin) + j0) * 2,
                            wd = (long(k.rpar) * cd.n_1 + dbase + j0) * 2;
                 uint32_t bytes = uint32_t(ncn) * NA * RC::RB + ring_words_bytes(wi, ncn * NA) + ring_words_bytes(ws, ncn * 2);
-                if constexpr (ND > 0) bytes += uint32_t(ncn) * 256u + (d1in ? ring_words_bytes(wd, ncn * 2) : 0u);
+                const int nblk = (j0 + ncn - (gs * SC - lo) + 7) >> 3;   // lam1 blocks of the stage
+                if constexpr (ND > 0) bytes += uint32_t(nblk) * 2048u + (d1in ? ring_words_bytes(wd, ncn * 2) : 0u);
                 mbar_expect_tx(bar, bytes);
                 tma_load_1d_ef(dst + RC::OFF_R, reinterpret_cast<const char*>(g.r) + size_t(abase + j0 * NA) * RC::RB,
                                uint32_t(ncn) * NA * RC::RB, bar, pol);
-                if constexpr (ND > 0)
-                    tma_load_1d_ef(dst + RC::OFF_L1, g.lam1 + size_t(dbase + j0) * 64, uint32_t(ncn) * 256u, bar, pol);
+                if constexpr (ND > 0)   // whole lam1 blocks from slot dbase + gs SC - lo (a multiple of 8)
+                    tma_load_1d_ef(dst + RC::OFF_L1, g.lam1 + size_t((dbase - lo) / 8 + gs * (SC / 8)) * 512, uint32_t(nblk) * 2048u,
+                                   bar, pol);
                 ring_copy_words(dst + RC::OFF_IDX, reinterpret_cast<const uint32_t*>(cd.a_vn), wi, ncn * NA, bar, pol);
                 ring_copy_words(dst + RC::OFF_SY, g.synd_t, ws, ncn * 2, bar, pol);
                 if constexpr (ND > 0)
@@ -944,12 +959,13 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
         int slot = 0;
         uint32_t phase = 0;   // parity of the slot's current use
         for (int gs = blockIdx.x; gs < nst; gs += gridDim.x) {
-            const int j0 = gs * SC, ncn = min(SC, count - j0);
+            const int j0 = max(gs * SC - lo, 0);
+            const int jl = gs * SC - lo + warp;          // class position of this warp's check
+            const int wl = jl - j0;                      // its index among the stage's copied rows
             mbar_wait(full_a + 8 * slot, phase);
-            if (warp < ncn) {
+            if (jl >= 0 && jl < count) {
                 const char* sp = ring + slot * RC::STG;
-                const int jl = j0 + warp;
-                const int* sidx = reinterpret_cast<const int*>(sp + RC::OFF_IDX) + ((abase + j0 * NA) & 3) + warp * NA;
+                const int* sidx = reinterpret_cast<const int*>(sp + RC::OFF_IDX) + ((abase + j0 * NA) & 3) + wl * NA;
                 uint32_t offs[NA];
                 float2 L2[NA], r2[NA];
 #pragma unroll
@@ -957,16 +973,16 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
                     offs[s] = uint32_t(sidx[s]) * 128u + uint32_t(lane);
                     L2[s] = make_float2(__ldg(g.L + offs[s]), __ldg(g.L + offs[s] + 32));   // L2-resident gathers
                 }
-                const uint32_t* ssy = reinterpret_cast<const uint32_t*>(sp + RC::OFF_SY) + (((begin + j0) * 2) & 3) + warp * 2;
+                const uint32_t* ssy = reinterpret_cast<const uint32_t*>(sp + RC::OFF_SY) + (((begin + j0) * 2) & 3) + wl * 2;
                 const uint32_t swx = ssy[0], swy = ssy[1];
                 uint2 wv = make_uint2(0, 0);
                 if constexpr (ND > 0)
                     if (d1in) {
                         const uint32_t* sd =
-                            reinterpret_cast<const uint32_t*>(sp + RC::OFF_D1) + ((long(k.rpar) * cd.n_1 + dbase + j0) * 2 & 3) + warp * 2;
+                            reinterpret_cast<const uint32_t*>(sp + RC::OFF_D1) + ((long(k.rpar) * cd.n_1 + dbase + j0) * 2 & 3) + wl * 2;
                         wv = make_uint2(sd[0], sd[1]);
                     }
-                const float* sr = reinterpret_cast<const float*>(sp + RC::OFF_R + warp * NA * RC::RB);
+                const float* sr = reinterpret_cast<const float*>(sp + RC::OFF_R + wl * NA * RC::RB);
 #pragma unroll
                 for (int s = 0; s < NA; ++s) {
                     if constexpr (MSG) r2[s] = msg16_q(reinterpret_cast<const uint32_t*>(sr)[s * 32 + lane]);
@@ -981,8 +997,9 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
                 }
                 float2 lam = make_float2(0.0f, 0.0f);
                 if constexpr (ND > 0) {
-                    const float* sl = reinterpret_cast<const float*>(sp + RC::OFF_L1 + warp * 256);
-                    lam = make_float2(sl[lane], sl[32 + lane]);
+                    const float* sl = reinterpret_cast<const float*>(sp + RC::OFF_L1 + (warp >> 3) * 2048) + lane * 8 +
+                                      ((warp & 7) ^ ((lane >> 2) & 7));
+                    lam = make_float2(sl[0], sl[256]);
                 }
                 void* pr = MSG ? static_cast<void*>(reinterpret_cast<unsigned int*>(g.r) + (size_t(abase + jl * NA) * 32 + lane))
                                : static_cast<void*>(g.r + (size_t(abase + jl * NA) * 64 + lane));
@@ -1081,7 +1098,7 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group 
                 chk ^= uint32_t(Lv < 0.0f);
             } else {
                 const int q = db + (s - na);
-                x = __ldcs(g.lam1 + size_t(q) * g.B + off);
+                x = __ldcs(g.lam1 + lam1_idx(q, int(off), g.B));
                 if (k.check) chk ^= (__ldg(g.d1bits + (size_t(k.rpar) * cd.n_1 + q) * g.C + c) >> lane) & 1u;
             }
             if (s < na) {
@@ -1340,7 +1357,7 @@ __global__ void __launch_bounds__(256) k_scatter(CodeDev cd, Group g, const floa
             g.L[size_t(v) * 2 * g.B + off] = lz;                     // L^0 = lambda (Step 2)
             g.L[size_t(v) * 2 * g.B + g.B + off] = 0.0f;             // empty VN-sum accumulator
         } else {
-            g.lam1[size_t(~v) * g.B + off] = lam1_phi_form(cd, val);
+            g.lam1[lam1_idx(~v, int(off), g.B)] = lam1_phi_form(cd, val);
         }
     }
 }
@@ -1687,7 +1704,7 @@ __global__ void __launch_bounds__(256) k_refill_scatter(CodeDev cd, Group g, Str
                 g.L[size_t(v) * 2 * g.B + b] = lz;
                 g.L[size_t(v) * 2 * g.B + g.B + b] = 0.0f;
             } else {
-                g.lam1[size_t(~v) * g.B + b] = lam1_phi_form(cd, val[u]);
+                g.lam1[lam1_idx(~v, b, g.B)] = lam1_phi_form(cd, val[u]);
             }
         }
     }
