@@ -1250,12 +1250,12 @@ metldpc_status metldpc_debug_dump(metldpc_decoder d, int32_t lane, float* r_out,
             r_out[L.perm_r[size_t(t)]] = float(int(tmp[size_t(t)]) - 0x8080) * (1.0f / 1024.0f);
     } else if (r_out && L.E_it) {   // device order (relabelled CNs) -> canonical active-edge CSR order
         std::vector<float> tmp(size_t(L.E_it));
-        CUDA_TRY(cudaMemcpy2D(tmp.data(), sizeof(float), d->ws[size_t(d->last_ws)].r + lane, size_t(d->B) * sizeof(float), sizeof(float),
+        CUDA_TRY(cudaMemcpy2D(tmp.data(), sizeof(float), d->ws[size_t(d->last_ws)].r + lpos(lane, d->B), size_t(d->B) * sizeof(float), sizeof(float),
                               size_t(L.E_it), cudaMemcpyDeviceToHost));
         for (int64_t t = 0; t < L.E_it; ++t) r_out[L.perm_r[size_t(t)]] = tmp[size_t(t)];
     }
     if (L_out && L.n_a)
-        CUDA_TRY(cudaMemcpy2D(L_out, sizeof(float), d->ws[size_t(d->last_ws)].L + lane, 2 * size_t(d->B) * sizeof(float), sizeof(float),
+        CUDA_TRY(cudaMemcpy2D(L_out, sizeof(float), d->ws[size_t(d->last_ws)].L + lpos(lane, d->B), 2 * size_t(d->B) * sizeof(float), sizeof(float),
                               size_t(L.n_a), cudaMemcpyDeviceToHost));
     return METLDPC_OK;
 }

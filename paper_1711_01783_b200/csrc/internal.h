@@ -26,7 +26,10 @@ constexpr uint32_t kPhiHiBits = uint32_t(127 + kPhiEHi) << 23;     // 2^6
 constexpr int kPhiZeroBinsExact = 1 << kPhiJExact, kPhiZeroBinsLut = 1 << kPhiJLut;
 // Device copy: each bin (plus one all-zero sentinel bin) replicated kPhiCopies times,
 // interleaved, so the 8 threads of a quarter-warp LDS phase read 8 distinct bank groups.
-constexpr int kPhiCopies = 8;
+#ifndef METLDPC_PHI_COPIES
+#define METLDPC_PHI_COPIES 8
+#endif
+constexpr int kPhiCopies = METLDPC_PHI_COPIES;
 
 void set_error(const std::string& msg);
 metldpc_status fail(metldpc_status s, const std::string& msg);

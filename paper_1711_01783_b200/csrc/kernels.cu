@@ -99,7 +99,7 @@ __device__ __forceinline__ float phi_dev(uint32_t tabk, float y, uint32_t one) {
 // in, held opaquely in one register (the bin offset then costs SHF + LEA).
 template <int RULE>
 __device__ __forceinline__ uint32_t phi_tab_lane(const char* smem, int lane) {
-    const uint32_t a = uint32_t(__cvta_generic_to_shared(smem)) + uint32_t((lane & 7) * PhiT<RULE>::ENTRY) -
+    const uint32_t a = uint32_t(__cvta_generic_to_shared(smem)) + uint32_t((lane & (kPhiCopies - 1)) * PhiT<RULE>::ENTRY) -
                        uint32_t(PhiT<RULE>::BIAS);
     uint32_t r;
     asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(a));
@@ -209,59 +209,6 @@ __device__ __forceinline__ uint32_t d1_decision(uint32_t nl, uint32_t nr, float 
     return nl ? (nr | uint32_t(p < S)) : (nr & uint32_t(S < p));
 }
 
-template <int RULE, int NA, int ND>
-__device__ __forceinline__ uint32_t cn_lane(uint32_t tabk, const float (&Lv)[NA > 0 ? NA : 1],
-                                            const float (&ro)[NA > 0 ? NA : 1], float lam, uint32_t sbit,
-                                            uint32_t d1prev, float* pr, float* pla, const uint32_t (&offs)[NA > 0 ? NA : 1],
-                                            const int* idx, bool act, uint32_t& d1bit) {
-    constexpr int D = NA + ND;
-    const uint32_t one = one_bits();
-    float p[D], P[D];
-    uint32_t xb[D];     // bits of x: sign bit = [x < 0] exactly (x is never -0, k_scatter), N1 / R2
-    uint32_t par = sbit << 31;                            // bit 31: s_j XOR all n_k
-    uint32_t chk = sbit ^ d1prev;
-#pragma unroll
-    for (int s = 0; s < NA; ++s) {
-        const float x = __fsub_rn(Lv[s], ro[s]);         // extrinsic q = L - r (R10)
-        chk ^= __float_as_uint(Lv[s]) >> 31;             // c_v^{l-1} = [L < 0]: L is never -0 (k_scatter)
-        xb[s] = __float_as_uint(x);
-        par ^= xb[s];
-        p[s] = phi_dev<RULE>(tabk, fabsf(x), one);
-    }
-    if constexpr (ND > 0) {          // degree-1 VN sends its prior, stored in phi form (N1)
-        xb[NA] = __float_as_uint(lam);                    // sign bit = [lambda < 0]
-        par ^= xb[NA];
-        p[NA] = fabsf(lam);                               // phi(|lambda|)
-    }
-    // P_0 = 0, P_{k+1} = P_k + p_k; Q_{D-1} = 0, Q_k = Q_{k+1} + p_{k+1}; S_k = P_k + Q_k.
-    // The additions with an exact +0 operand are skipped: p, P, Q >= +0, so 0 + v = v.
-    P[0] = 0.0f;
-    if constexpr (D > 1) P[1] = p[0];
-#pragma unroll
-    for (int s = 2; s < D; ++s) P[s] = __fadd_rn(P[s - 1], p[s - 1]);
-    float Q = 0.0f;
-#pragma unroll
-    for (int s = D - 1; s >= 0; --s) {
-        const float S = (s == D - 1) ? P[s] : (s == 0 ? Q : __fadd_rn(P[s], Q));
-        if (s >= NA) {   // Step 5 for the degree-1 VN: sign of lambda + rho, decided as N1 (no phi(S))
-            d1bit = d1_decision(xb[s], par ^ xb[s], p[s], S);
-            if (s > 0) Q = __fadd_rn(Q, p[s]);
-            continue;
-        }
-        const float mag = fminf(phi_dev<RULE>(tabk, S, one), kRMax);
-        const float o = __uint_as_float(__float_as_uint(mag) | ((par ^ xb[s]) & 0x80000000u));
-        {
-            (void)act;   // unpredicated, as in cn_pair
-            __stcs(pr + s * 64, o);
-            // VN sum (Eq. 4); row offsets from registers for small NA, from shared memory otherwise
-            const uint32_t ro_s = (NA <= 4) ? offs[s] : uint32_t(idx[s]);
-            atomicAdd(reinterpret_cast<unsigned int*>(pla + ro_s + 64), vn_fix(o));
-        }
-        if (s > 0) Q = __fadd_rn(Q, p[s]);
-    }
-    return chk;
-}
-
 // ------------------------------------------------------------------ two-lane (fp32x2) helpers
 
 // sm_100a packed fp32 pairs: FADD2 / FFMA2 round each element to nearest like FADD / FFMA,
@@ -323,8 +270,12 @@ __device__ __forceinline__ float2 phi_pair(uint32_t tabk, float y0, float y1, ui
     return r;
 }
 
-// DESIGN.md N1 for one CN and the two lanes (l, l + 32) of a thread, element-wise
-// identical to cn_lane (same fp32 operations, pairs where the two lanes do the same op).
+// DESIGN.md N1 for one CN and the two lanes (l, l + 32) of a thread (slot order: actives, then the
+// degree-1 slot; Eqs. (2)-(3), in sign/phi form with the syndrome sign, R1), the two
+// lanes' identical fp32 operations as packed pairs.  Returns the syndrome-test bits (N4) of
+// iteration l - 1; stores r for the active slots and returns the degree-1 decision bits.
+// Fixed-point VN-sum term of a message (N3): bits(fmaf(o, 2^17, 1.5 * 2^23)) = 0x4B400000 +
+// rint(2^17 o) exactly for |2^17 o| < 2^22 (|o| <= 30); the finish kernel removes the bias.
 // 16-bit message storage (R28 / N7), the two lanes of a thread in one 32-bit word
 // (lane l in the low half, lane l + 32 in the high half).  A stored half-word is w = q + 0x8080
 // for the message q * 2^-10, q = rint(2^10 o): fmaf(o, 2^10, 2^23 + 0x8080) = 2^23 + w exactly
@@ -406,38 +357,24 @@ __device__ __forceinline__ uint2 cn_pair(uint32_t tabk, const float2 (&Lv)[NA > 
             // read for that lane again (k_finish keeps its L and clears the accumulator), and
             // full 256-byte rows avoid partial-sector writes.
             const float2 fx = f2fma(o, make_float2(131072.0f, 131072.0f), make_float2(12582912.0f, 12582912.0f));
-            unsigned int* pa = reinterpret_cast<unsigned int*>(pla + offs[s] + 64);
-            if constexpr (MSG) {
-                __stcs(reinterpret_cast<unsigned int*>(prv) + s * 32, msg16_pack(o));   // stored message (N7)
-                atomicAdd(pa, __float_as_uint(fx.x));              // VN sum of the unrounded o (Eq. 4, N3)
-                atomicAdd(pa + 32, __float_as_uint(fx.y));
-            } else {
-                __stcs(pr + s * 64, o.x);
-                atomicAdd(pa, __float_as_uint(fx.x));              // VN sum (Eq. 4, N3)
-                __stcs(pr + s * 64 + 32, o.y);
-                atomicAdd(pa + 32, __float_as_uint(fx.y));
-            }
+            // VN sums of both lanes (Eq. 4, N3; of the unrounded o with 16-bit storage) in one
+            // 64-bit RED on the thread's pair word of the accumulator row (offs = pair position)
+            atomicAdd(reinterpret_cast<unsigned long long*>(pla + offs[s] + 64),
+                      (static_cast<unsigned long long>(__float_as_uint(fx.y)) << 32) | __float_as_uint(fx.x));
+            if constexpr (MSG) __stcs(reinterpret_cast<unsigned int*>(prv) + s * 32, msg16_pack(o));   // stored message (N7)
+            else __stcs(reinterpret_cast<float2*>(pr) + s * 32, o);                            // pair row: lanes l, l + 32
         }
         if (s > 0) Q = f2add(Q, p[s]);
     }
     return make_uint2((lw0 >> 31) ^ sbit.x ^ d1prev.x, (lw1 >> 31) ^ sbit.y ^ d1prev.y);
 }
 
-#ifndef METLDPC_CN_PAIR
-#define METLDPC_CN_PAIR 1   // two-lane path with packed fp32x2 ops (FADD2 / FFMA2)
-#endif
-
 // One degree class (CN labels [begin, begin + count), NA active + ND <= 1 degree-1 slots)
 // for 64-lane groups.  Work unit = a tile of ts consecutive CNs owned by one warp that
 // covers both 32-lane chunks (each thread: lanes `lane` and `lane + 32`, two independent
-// dependency chains; NA > 4 runs 1 CTA per SM with up to 128 registers).  With
-// METLDPC_PAIR_MAX_NA < NA a unit is one chunk instead (the latency-bound core classes
-// measured ~2 % faster with two lanes per thread).
+// dependency chains; NA > 4 runs 1 CTA per SM with up to 128 registers).
 // The tile's metadata is one coalesced load per array and its active-edge VN indices
 // (pre-scaled to row offsets) are staged in shared memory.
-#ifndef METLDPC_PAIR_MAX_NA
-#define METLDPC_PAIR_MAX_NA 16  // largest active count run two lanes per thread in k_cn_tile
-#endif
 template <int NA>
 __host__ __device__ constexpr int cn_tile_min_blocks() { return NA <= 4 ? 2 : 1; }   // NA > 4: 128 registers
 
@@ -445,8 +382,7 @@ template <int RULE, int NA, int ND, int MSG = 0>
 __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_tile(CodeDev cd, Group g, CnCtl karg,
                                                                                   int begin, int count, int ts) {
     using PT = PhiT<RULE>;
-    constexpr int LPT = (NA <= METLDPC_PAIR_MAX_NA) ? 2 : 1;     // lanes per thread
-    static_assert(!MSG || (LPT == 2 && METLDPC_CN_PAIR), "16-bit rows: two lanes per thread, pair path");
+    constexpr int LPT = 2;                     // lanes l and l + 32 per thread (pair rows)
     constexpr int UPT = 2 / LPT;               // units per tile
     constexpr int NAS = NA > 0 ? NA : 1;
     constexpr int STAGE = (NA <= 4 ? 32 : 8) * NAS;
@@ -501,26 +437,23 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
                 const int q0 = __shfl_sync(FULL, d_l, i);
                 const uint32_t swx = __shfl_sync(FULL, sw_l.x, i), swy = __shfl_sync(FULL, sw_l.y, i);
                 const int* idx = s_idx + (ab - A0);
-                const uint32_t lo = uint32_t(c0 * 32 + lane);
-                float* pL = g.L + lo;
-                float* pr = g.r + (size_t(ab) * 64 + lo);
+                float* pr = g.r + (size_t(ab) * 64 + 2 * lane);   // pair rows: lanes lane, lane + 32 adjacent
                 float Lv[LPT][NAS], ro[LPT][NAS], lam[LPT];
-                uint32_t offs[NAS];   // NA <= 4: row offset + lane as one unsigned index (one IMAD.WIDE.U32)
-                uint32_t w[LPT];
+                uint32_t offs[NAS];   // pair position of the thread in the VN's row (one IMAD.WIDE.U32 per gather)
 #pragma unroll
                 for (int s = 0; s < NA; ++s) {
-                    const int o = idx[s];
-                    if constexpr (NA <= 4 || LPT == 2) offs[s] = uint32_t(o) + lo;
-#pragma unroll
-                    for (int h = 0; h < LPT; ++h)
-                        Lv[h][s] = (NA <= 4) ? __ldg(g.L + offs[s] + h * 32) : __ldg(pL + o + h * 32);
+                    offs[s] = uint32_t(idx[s]) + 2u * uint32_t(lane);
+                    const float2 lv = __ldg(reinterpret_cast<const float2*>(g.L + offs[s]));
+                    Lv[0][s] = lv.x;
+                    Lv[1][s] = lv.y;
                     if constexpr (MSG) {   // 16-bit row: the thread's word holds lanes lane, lane + 32 (N7)
                         const float2 q = msg16_q(__ldcs(reinterpret_cast<const unsigned int*>(g.r) + size_t(ab + s) * 32 + lane));
                         ro[0][s] = q.x;
-                        ro[LPT - 1][s] = q.y;
+                        ro[1][s] = q.y;
                     } else {
-#pragma unroll
-                        for (int h = 0; h < LPT; ++h) ro[h][s] = __ldcs(pr + s * 64 + h * 32);   // r^0 = 0: zeroed at group begin
+                        const float2 q = __ldcs(reinterpret_cast<const float2*>(pr) + s * 32);   // r^0 = 0: zeroed at group begin
+                        ro[0][s] = q.x;
+                        ro[1][s] = q.y;
                     }
                 }
                 if (s_fresh[0] | s_fresh[1]) {   // lane refill: r^0 = 0 for a frame starting in this pass
@@ -540,7 +473,7 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
                     for (int h = 0; h < LPT; ++h) lam[h] = 0.0f;
                 }
                 uint32_t chk[LPT], b[LPT];
-                if constexpr (LPT == 2 && METLDPC_CN_PAIR) {
+                {
                     float2 L2[NAS], r2[NAS];
 #pragma unroll
                     for (int s = 0; s < NA; ++s) {
@@ -557,17 +490,6 @@ __global__ void __launch_bounds__(kCnThreads, cn_tile_min_blocks<NA>()) k_cn_til
                     chk[1] = c2.y;
                     b[0] = d1.x;
                     b[1] = d1.y;
-                } else {
-#pragma unroll
-                for (int h = 0; h < LPT; ++h) {
-                    const int c = c0 + h;
-                    const uint32_t sbit = ((c ? swy : swx) >> lane) & 1u;
-                    w[h] = (((c ? wv.y : wv.x) >> lane) & 1u);
-                    const bool act = (((c ? am1 : am0) >> lane) & 1u) != 0u;
-                    b[h] = 0;
-                    chk[h] = cn_lane<RULE, NA, ND>(tabk, Lv[h], ro[h], lam[h], sbit, w[h], pr + h * 32,
-                                                   (NA <= 4 ? g.L : pL) + h * 32, offs, idx, act, b[h]);
-                }
                 }
 #pragma unroll
                 for (int h = 0; h < LPT; ++h) {
@@ -770,15 +692,15 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND, MSG>::THREADS, 1)
             float2 L2[NA], r2[NA];
 #pragma unroll
             for (int s = 0; s < NA; ++s) {
-                offs[s] = uint32_t(idx[s]) + uint32_t(lane);
-                L2[s] = make_float2(__ldg(g.L + offs[s]), __ldg(g.L + offs[s] + 32));   // L2-resident gathers
+                offs[s] = uint32_t(idx[s]) + 2u * uint32_t(lane);
+                L2[s] = __ldg(reinterpret_cast<const float2*>(g.L + offs[s]));   // L2-resident gathers, pair rows
             }
             mbar_wait(bar_a + 8 * st, ph);
             const float* sr = reinterpret_cast<const float*>(stage + st * PC::STG);
 #pragma unroll
             for (int s = 0; s < NA; ++s) {
                 if constexpr (MSG) r2[s] = msg16_q(reinterpret_cast<const uint32_t*>(sr)[s * 32 + lane]);   // q (N7)
-                else r2[s] = make_float2(sr[s * 64 + lane], sr[s * 64 + 32 + lane]);
+                else r2[s] = reinterpret_cast<const float2*>(sr + s * 64)[lane];
             }
             // r^0 = 0 for a lane whose frame starts in this pass (Step 2), applied in registers:
             // the ring stages are written only by the TMA (async proxy), never by the threads
@@ -794,7 +716,7 @@ __global__ void __launch_bounds__(PipeCfg<NA, ND, MSG>::THREADS, 1)
             if constexpr (ND > 0)   // blocked lam1 rows: two direct loads (this kernel is the METLDPC_RING=0 path)
                 lam = make_float2(__ldcs(g.lam1 + lam1_idx(dbase + jl, lane, 64)), __ldcs(g.lam1 + lam1_idx(dbase + jl, lane + 32, 64)));
             void* pr = MSG ? static_cast<void*>(reinterpret_cast<unsigned int*>(g.r) + (size_t(abase + jl * NA) * 32 + lane))
-                           : static_cast<void*>(g.r + (size_t(abase + jl * NA) * 64 + lane));
+                           : static_cast<void*>(g.r + (size_t(abase + jl * NA) * 64 + 2 * lane));
             uint2 d1 = make_uint2(0, 0);
             const uint2 c2 = cn_pair<RULE, NA, ND, MSG>(tabk, L2, r2, lam, make_uint2((swx >> lane) & 1u, (swy >> lane) & 1u),
                                                         make_uint2((wv.x >> lane) & 1u, (wv.y >> lane) & 1u), pr, g.L, offs, d1);
@@ -970,8 +892,8 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
                 float2 L2[NA], r2[NA];
 #pragma unroll
                 for (int s = 0; s < NA; ++s) {
-                    offs[s] = uint32_t(sidx[s]) * 128u + uint32_t(lane);
-                    L2[s] = make_float2(__ldg(g.L + offs[s]), __ldg(g.L + offs[s] + 32));   // L2-resident gathers
+                    offs[s] = uint32_t(sidx[s]) * 128u + 2u * uint32_t(lane);
+                    L2[s] = __ldg(reinterpret_cast<const float2*>(g.L + offs[s]));   // L2-resident gathers, pair rows
                 }
                 const uint32_t* ssy = reinterpret_cast<const uint32_t*>(sp + RC::OFF_SY) + (((begin + j0) * 2) & 3) + wl * 2;
                 const uint32_t swx = ssy[0], swy = ssy[1];
@@ -986,7 +908,7 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
 #pragma unroll
                 for (int s = 0; s < NA; ++s) {
                     if constexpr (MSG) r2[s] = msg16_q(reinterpret_cast<const uint32_t*>(sr)[s * 32 + lane]);
-                    else r2[s] = make_float2(sr[s * 64 + lane], sr[s * 64 + 32 + lane]);
+                    else r2[s] = reinterpret_cast<const float2*>(sr + s * 64)[lane];
                 }
                 if (any_fresh) {   // r^0 = 0 for a frame starting in this pass (Step 2), in registers
 #pragma unroll
@@ -1002,7 +924,7 @@ __global__ void __launch_bounds__(RingCfg<NA, ND, MSG>::THREADS, 1)
                     lam = make_float2(sl[0], sl[256]);
                 }
                 void* pr = MSG ? static_cast<void*>(reinterpret_cast<unsigned int*>(g.r) + (size_t(abase + jl * NA) * 32 + lane))
-                               : static_cast<void*>(g.r + (size_t(abase + jl * NA) * 64 + lane));
+                               : static_cast<void*>(g.r + (size_t(abase + jl * NA) * 64 + 2 * lane));
                 uint2 d1 = make_uint2(0, 0);
                 const uint2 c2 = cn_pair<RULE, NA, ND, MSG>(tabk, L2, r2, lam,
                                                             make_uint2((swx >> lane) & 1u, (swy >> lane) & 1u),
@@ -1071,9 +993,12 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group 
     for (long item = long(blockIdx.x) * wpb + (threadIdx.x >> 5); item < total; item += long(gridDim.x) * wpb) {
         const int c = int(item & (g.C - 1));
         const uint32_t amask = s_act[c];
-        if (!amask) continue;
+        // a chunk is skipped only with its pair chunk: every lane of a pair word must receive its
+        // VN's deg terms for the 64-bit accumulator to decode (k_finish)
+        if (!(amask | (g.B == 32 ? 0u : s_act[c ^ 1]))) continue;
         const int j = begin + int(item >> lc);
         const size_t off = size_t(c) * 32 + lane;
+        const size_t po = size_t(lpos(int(off), g.B));   // pair position of the lane (r, L, accumulator rows)
         const int ab = __ldg(cd.cn_aptr + j), na = __ldg(cd.cn_aptr + j + 1) - ab;
         const int db = __ldg(cd.cn_dptr + j), d = na + (__ldg(cd.cn_dptr + j + 1) - db);
         const uint32_t sbit = (__ldg(g.synd_t + size_t(j) * g.C + c) >> lane) & 1u;
@@ -1085,14 +1010,14 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group 
             float x;
             if (s < na) {
                 const int v = __shfl_sync(FULL, idx, s);
-                const float Lv = __ldg(g.L + size_t(v) * 2 * g.B + off);
+                const float Lv = __ldg(g.L + size_t(v) * 2 * g.B + po);
                 if (g.msg16) {   // 16-bit row (N7): half-word c of word `lane`; x = L - q 2^-10 (one rounding)
                     const uint32_t w = ((g.fresh[c] >> lane) & 1u) ? 0x8080u
                         : uint32_t(__ldcs(reinterpret_cast<const unsigned short*>(g.r) + size_t(ab + s) * 64 + 2 * lane + c));
                     const float q = __fsub_rn(__uint_as_float(0x4B000000u | w), kMsg16Magic);
                     x = __fmaf_rn(q, -0.0009765625f, Lv);
                 } else {
-                    const float ro = ((g.fresh[c] >> lane) & 1u) ? 0.0f : __ldcs(g.r + size_t(ab + s) * g.B + off);
+                    const float ro = ((g.fresh[c] >> lane) & 1u) ? 0.0f : __ldcs(g.r + size_t(ab + s) * g.B + po);
                     x = __fsub_rn(Lv, ro);
                 }
                 chk ^= uint32_t(Lv < 0.0f);
@@ -1134,13 +1059,19 @@ __global__ void __launch_bounds__(kCnThreads, 2) k_cn_generic(CodeDev cd, Group 
             const float o = __uint_as_float(__float_as_uint(mag) | ((par ^ ((negmask >> s) & 1u)) << 31));
             {
                 const int v = __shfl_sync(FULL, idx, s);      // whole warp: lane s may be an idle lane
-                if (act) {
+                {   // unpredicated, as the pair kernels: each lane's accumulator gets exactly deg terms
+                    (void)act;
                     if (g.msg16)
                         __stcs(reinterpret_cast<unsigned short*>(g.r) + size_t(ab + s) * 64 + 2 * lane + c,
                                (unsigned short)(__float_as_uint(__fmaf_rn(o, 1024.0f, kMsg16Magic)) & 0xFFFFu));
                     else
-                        __stcs(g.r + size_t(ab + s) * g.B + off, o);
-                    atomicAdd(reinterpret_cast<unsigned int*>(g.L + size_t(v) * 2 * g.B + g.B + off), vn_fix(o));
+                        __stcs(g.r + size_t(ab + s) * g.B + po, o);
+                    float* acc = g.L + size_t(v) * 2 * g.B + g.B;
+                    if (g.B == 32)
+                        atomicAdd(reinterpret_cast<unsigned int*>(acc + off), vn_fix(o));
+                    else   // the lane's half of its pair word, as a 64-bit add (the same sum as the pair kernels' REDs)
+                        atomicAdd(reinterpret_cast<unsigned long long*>(acc + (po & ~size_t(1))),
+                                  static_cast<unsigned long long>(vn_fix(o)) << (32 * (po & 1)));
                 }
             }
             if (s > 0) Q = __fadd_rn(Q, p[s]);
@@ -1169,7 +1100,8 @@ __global__ void __launch_bounds__(256) k_check(CodeDev cd, Group g, int par) {
         const int ab = __ldg(cd.cn_aptr + j), ae = __ldg(cd.cn_aptr + j + 1);
         const int db = __ldg(cd.cn_dptr + j), de = __ldg(cd.cn_dptr + j + 1);
         uint32_t chk = (__ldg(g.synd_t + size_t(j) * g.C + c) >> lane) & 1u;
-        for (int t = ab; t < ae; ++t) chk ^= uint32_t(__ldg(g.L + size_t(__ldg(cd.a_vn + t)) * 2 * g.B + off) < 0.0f);
+        const int po = lpos(int(off), g.B);
+        for (int t = ab; t < ae; ++t) chk ^= uint32_t(__ldg(g.L + size_t(__ldg(cd.a_vn + t)) * 2 * g.B + po) < 0.0f);
         for (int q = db; q < de; ++q) chk ^= (__ldg(g.d1bits + (size_t(par) * cd.n_1 + q) * g.C + c) >> lane) & 1u;
         const uint32_t mm = __ballot_sync(FULL, chk) & amask;
         if (mm && lane == 0) atomicOr(&s_unsat[c], mm);
@@ -1201,14 +1133,34 @@ __global__ void __launch_bounds__(256) k_finish(CodeDev cd, Group g) {
         uint4* Arow = reinterpret_cast<uint4*>(g.L + size_t(a) * 2 * g.B + g.B);
         const uint4 acc = Arow[q];
         const float4 lam = __ldg(reinterpret_cast<const float4*>(g.lam_a + size_t(a) * g.B) + q);
-        const int b0 = q * 4;
-        const uint32_t m = (s_act[b0 >> 5] >> (b0 & 31)) & 0xFu;
+        // positions 4q .. 4q + 3 of the pair rows; their lanes and fixed-point sums
+        int sx, sy, sz, sw;
+        uint32_t m;
+        if (g.B == 32) {
+            m = (s_act[0] >> (q * 4)) & 0xFu;
+            sx = int(acc.x - bias);
+            sy = int(acc.y - bias);
+            sz = int(acc.z - bias);
+            sw = int(acc.w - bias);
+        } else {
+            // words (x, y) and (z, w): lanes t, t + 32 and t + 1, t + 33 of the 64-lane block
+            const int blk = (q * 4) & ~63, t = ((q * 4) & 63) >> 1;
+            const uint32_t lo = s_act[blk >> 5] >> t, hi = s_act[(blk >> 5) + 1] >> t;
+            m = (lo & 1u) | ((hi & 1u) << 1) | ((lo & 2u) << 1) | ((hi & 2u) << 2);
+            // 64-bit word = (deg bias + sum_hi) 2^32 + (deg bias + sum_lo) mod 2^64: the low sum
+            // is exact mod 2^32 (|sum| < 2^31), and its carry into the high word follows from it
+            const unsigned long long dB = static_cast<unsigned long long>(uint32_t(deg)) * 0x4B400000ull;
+            sx = int(acc.x - bias);
+            sy = int(acc.y - bias - uint32_t((dB + static_cast<unsigned long long>(static_cast<long long>(sx))) >> 32));
+            sz = int(acc.z - bias);
+            sw = int(acc.w - bias - uint32_t((dB + static_cast<unsigned long long>(static_cast<long long>(sz))) >> 32));
+        }
         float4 L = (m == 0xFu) ? make_float4(0.f, 0.f, 0.f, 0.f) : Lrow[q];   // all 4 lanes rewritten: skip the read
         const float sc = 1.0f / 131072.0f;
-        if (m & 1u) L.x = __fadd_rn(lam.x, __fmul_rn(__int2float_rn(int(acc.x - bias)), sc));
-        if (m & 2u) L.y = __fadd_rn(lam.y, __fmul_rn(__int2float_rn(int(acc.y - bias)), sc));
-        if (m & 4u) L.z = __fadd_rn(lam.z, __fmul_rn(__int2float_rn(int(acc.z - bias)), sc));
-        if (m & 8u) L.w = __fadd_rn(lam.w, __fmul_rn(__int2float_rn(int(acc.w - bias)), sc));
+        if (m & 1u) L.x = __fadd_rn(lam.x, __fmul_rn(__int2float_rn(sx), sc));
+        if (m & 2u) L.y = __fadd_rn(lam.y, __fmul_rn(__int2float_rn(sy), sc));
+        if (m & 4u) L.z = __fadd_rn(lam.z, __fmul_rn(__int2float_rn(sz), sc));
+        if (m & 8u) L.w = __fadd_rn(lam.w, __fmul_rn(__int2float_rn(sw), sc));
         if (m) Lrow[q] = L;
         Arow[q] = make_uint4(0u, 0u, 0u, 0u);
     }
@@ -1225,7 +1177,7 @@ __global__ void __launch_bounds__(256) k_check64(CodeDev cd, Group g, int par) {
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     const int ntiles = (cd.m + 31) >> 5;
-    const float* Ll = g.L + lane;
+    const float* Ll = g.L + 2 * lane;   // pair rows: lanes lane, lane + 32 adjacent
     uint32_t un0 = 0, un1 = 0;
     if (am0 | am1) {
         for (int tile = blockIdx.x * wpb + (threadIdx.x >> 5); tile < ntiles; tile += gridDim.x * wpb) {
@@ -1243,8 +1195,9 @@ __global__ void __launch_bounds__(256) k_check64(CodeDev cd, Group g, int par) {
                 const int idx = (lane < na) ? __ldg(cd.a_vn + ab + lane) * 128 : 0;
                 for (int s = 0; s < na; ++s) {
                     const int o = __shfl_sync(FULL, idx, s);
-                    c0 ^= uint32_t(__ldg(Ll + o) < 0.0f);
-                    c1 ^= uint32_t(__ldg(Ll + o + 32) < 0.0f);
+                    const float2 lv = __ldg(reinterpret_cast<const float2*>(Ll + o));
+                    c0 ^= uint32_t(lv.x < 0.0f);
+                    c1 ^= uint32_t(lv.y < 0.0f);
                 }
                 for (int q = db; q < db + nd; ++q) {
                     const uint2 w = __ldg(reinterpret_cast<const uint2*>(g.d1bits) + (size_t(par) * cd.n_1 + q));
@@ -1353,9 +1306,10 @@ __global__ void __launch_bounds__(256) k_scatter(CodeDev cd, Group g, const floa
             // and no extrinsic L - r is ever -0 (L^l = lambda + sum, x = L - r with L != -0), so
             // the CN kernels read [L < 0] and [x < 0] straight from the sign bits.
             const float lz = __fadd_rn(val, 0.0f);
-            g.lam_a[size_t(v) * g.B + off] = lz;
-            g.L[size_t(v) * 2 * g.B + off] = lz;                     // L^0 = lambda (Step 2)
-            g.L[size_t(v) * 2 * g.B + g.B + off] = 0.0f;             // empty VN-sum accumulator
+            const int po = lpos(int(off), g.B);
+            g.lam_a[size_t(v) * g.B + po] = lz;
+            g.L[size_t(v) * 2 * g.B + po] = lz;                      // L^0 = lambda (Step 2)
+            g.L[size_t(v) * 2 * g.B + g.B + po] = 0.0f;              // empty VN-sum accumulator (its half)
         } else {
             g.lam1[lam1_idx(~v, int(off), g.B)] = lam1_phi_form(cd, val);
         }
@@ -1435,7 +1389,7 @@ __global__ void __launch_bounds__(256) k_finalize(CodeDev cd, Group g, int nb, u
         const int v = __ldg(cd.vmap + i);
         uint32_t b;
         if (v >= 0) {
-            b = g.L[size_t(v) * 2 * g.B + off] < 0.0f;
+            b = g.L[size_t(v) * 2 * g.B + lpos(int(off), g.B)] < 0.0f;
         } else {
             const uint32_t w0 = g.d1bits[(size_t(0) * cd.n_1 + ~v) * g.C + c];
             const uint32_t w1 = g.d1bits[(size_t(1) * cd.n_1 + ~v) * g.C + c];
@@ -1600,7 +1554,7 @@ __global__ void __launch_bounds__(256) k_finalize_lanes(CodeDev cd, Group g, Str
             const int b = s_b[q], c = b >> 5;
             const int par = g.lane_fbuf[b];
             uint32_t bit = 0;
-            if (act) bit = Lv[b] < 0.0f;
+            if (act) bit = Lv[lpos(b, g.B)] < 0.0f;
             else if (d1) bit = (g.d1bits[size_t(par) * cd.n_1 * g.C + d1off + c] >> (b & 31)) & 1u;
             bits[u] = bit;
         }
@@ -1700,9 +1654,10 @@ __global__ void __launch_bounds__(256) k_refill_scatter(CodeDev cd, Group g, Str
             const int v = vm[u];
             if (v >= 0) {
                 const float lz = __fadd_rn(val[u], 0.0f);   // -0 -> +0, as k_scatter
-                g.lam_a[size_t(v) * g.B + b] = lz;
-                g.L[size_t(v) * 2 * g.B + b] = lz;
-                g.L[size_t(v) * 2 * g.B + g.B + b] = 0.0f;
+                const int po = lpos(b, g.B);
+                g.lam_a[size_t(v) * g.B + po] = lz;
+                g.L[size_t(v) * 2 * g.B + po] = lz;
+                g.L[size_t(v) * 2 * g.B + g.B + po] = 0.0f;
             } else {
                 g.lam1[lam1_idx(~v, b, g.B)] = lam1_phi_form(cd, val[u]);
             }
@@ -2055,7 +2010,7 @@ static void cn_pipe_geom(int rule, int D, int nd, int msg16, int* threads, size_
 }
 
 int cn_tile_max(int D, int nd) { return (D - nd) <= 4 ? 32 : 8; }
-int cn_units_per_tile(int D, int nd) { return (D - nd) <= METLDPC_PAIR_MAX_NA ? 1 : 2; }
+int cn_units_per_tile(int, int) { return 1; }
 
 size_t cn_smem(int rule, int D, int nd) {
     const size_t tab = size_t(rule == METLDPC_RULE_EXACT ? PhiT<METLDPC_RULE_EXACT>::TAB_BYTES

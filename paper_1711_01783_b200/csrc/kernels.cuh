@@ -5,6 +5,14 @@
 
 namespace metldpc {
 
+// Position of lane b in a "pair" row (r rows and the VN-sum accumulator rows): inside each block
+// of 64 lanes, lanes t and t + 32 are adjacent (word t of the thread that carries both lanes), so
+// a thread moves its two lanes with one 8-byte access and adds both fixed-point terms with one
+// 64-bit RED (N3, section 6).  32-lane groups keep lane order.
+__host__ __device__ __forceinline__ int lpos(int b, int B) {
+    return B == 32 ? b : (b & ~63) | ((b & 31) << 1) | ((b >> 5) & 1);
+}
+
 // Device state of the lane group being decoded.  Arrays are codeword-interleaved:
 // element (slot s, lane b) lives at s * B + b, B = lanes per group (32/64/128), so
 // a warp (32 consecutive lanes) touches one full 128-byte line per slot
@@ -14,10 +22,13 @@ namespace metldpc {
 struct Group {
     int B, C;
     int msg16;         // 1: r rows hold 16-bit messages (N7; 64-lane groups only)
-    float* r;          // [E_it][B]   CN->VN messages r_ji of active edges (Eqs. 2-3); with msg16
-                       //             [E_it][32] uint32 words, word t = lanes t (low), t + 32 (high)
-    float* L;          // [n_a][2][B] row of VN a: posterior LLR L (Eq. 5) at +0, the fixed-point
-                       //             accumulator of the next L (uint32, N3) at +B
+    float* r;          // [E_it][B]   CN->VN messages r_ji of active edges (Eqs. 2-3), lane b at
+                       //             lpos(b); with msg16 [E_it][32] uint32 words, word t = lanes t
+                       //             (low), t + 32 (high) -- the same pair order
+    float* L;          // [n_a][2][B] row of VN a: posterior LLR L (Eq. 5) at +0 (lane order), the
+                       //             fixed-point accumulator of the next L at +B: B = 32 uint32 per
+                       //             lane; B = 64 / 128 one uint64 per lane pair (t, t + 32) of each
+                       //             64-lane block, low word lane t (N3)
     float* lam_a;      // [n_a][B]    channel LLR of active VNs (Eq. 1)
     float* lam1;       // [n_1][B]    degree-1 priors in phi form: phi(|lambda|), sign bit [lambda < 0]
                        //             (N1), CSR slot order
