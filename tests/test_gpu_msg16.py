@@ -82,16 +82,17 @@ def test_c1_msg16_bits_iters_flags(c1, rule, refill):
 @pytest.mark.parametrize("rule", RULES)
 def test_c1_msg16_messages_every_iteration(c1, rule):
     code, h = c1
-    fr = _mixed(code, [(0.161, 2), (0.3, 2)], key=71)
+    fr = _mixed(code, [(0.161, 18), (0.3, 18)], key=71)
     llr = _llr(fr)
+    lanes = (0, 1, 17, 18, 32, 33, 34, 35)   # both halves of the pair words (N3, N7)
     N = 30
-    traces = [bp.decode(code, llr[i], fr["synd"][i], N, early_term=False, rule=rule, prec=32, trace=True, msg16=True)
-              for i in range(len(llr))]
+    traces = {i: bp.decode(code, llr[i], fr["synd"][i], N, early_term=False, rule=rule, prec=32, trace=True, msg16=True)
+              for i in lanes}
     dec = B.Decoder(h, len(llr), rule=rule, max_iter=N, early_term=False, msg_bits=16)
     L_t, S_t = torch.from_numpy(llr).cuda(), torch.from_numpy(fr["synd"].view(np.int32)).cuda()
     for l in range(1, N + 1):
         dec.decode(L_t, S_t, max_iter=l)
-        for i in range(len(llr)):
+        for i in lanes:
             r, L = dec.dump(i)
             assert np.array_equal(r.view(np.uint32), traces[i]["r_trace"][l - 1].view(np.uint32)), (l, i)
             assert np.array_equal(L.view(np.uint32), traces[i]["L_trace"][l - 1].view(np.uint32)), (l, i)

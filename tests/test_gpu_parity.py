@@ -100,19 +100,21 @@ def test_c1_bits_iters_flags_bit_exact(c1, rule):
 
 @pytest.mark.parametrize("rule", RULES)
 def test_c1_messages_every_iteration(c1, rule):
-    """r^l and L^l of every lane bit-identical to the oracle's trace for l = 1..N (ET off)."""
+    """r^l and L^l bit-identical to the oracle's trace for l = 1..N (ET off), for lanes in both
+    halves of the pair rows (lanes t and t + 32 share a 64-bit accumulator word, N3)."""
     code, h = c1
-    fr = _frames(code, [(0.161, 2), (0.3, 2)])
+    fr = _frames(code, [(0.161, 18), (0.3, 18)])
     llr = _llr_oracle(fr)
+    lanes = (0, 1, 17, 18, 32, 33, 34, 35)   # frame i decodes in lane i
     N = 40
-    traces = [bp.decode(code, llr[i], fr["synd"][i], N, early_term=False, rule=rule, prec=32, trace=True)
-              for i in range(len(llr))]
+    traces = {i: bp.decode(code, llr[i], fr["synd"][i], N, early_term=False, rule=rule, prec=32, trace=True)
+              for i in lanes}
     dec = B.Decoder(h, len(llr), rule=rule, max_iter=N, early_term=False)
     L_t = torch.from_numpy(llr).cuda()
     S_t = torch.from_numpy(fr["synd"].view(np.int32)).cuda()
     for l in range(1, N + 1):
         dec.decode(L_t, S_t, max_iter=l)
-        for i in range(len(llr)):
+        for i in lanes:
             r, L = dec.dump(i)
             assert np.array_equal(r.view(np.uint32), traces[i]["r_trace"][l - 1].view(np.uint32)), (l, i)
             assert np.array_equal(L.view(np.uint32), traces[i]["L_trace"][l - 1].view(np.uint32)), (l, i)
