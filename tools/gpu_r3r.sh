@@ -1,0 +1,14 @@
+#!/bin/bash
+# GPU call: refill wave in three launches (persistent finalize; scatter + S_B + activate fused): parity, wave cost, headline A/B
+set -x
+O=gpurun_out/r3r; mkdir -p $O
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_paths.py tests/test_gpu_msg16.py -x -q -k "refill or streaming or host or headline or edge or invariance" > $O/pytest_refill.log 2>&1; echo "rc=$?" >> $O/pytest_refill.log
+timeout 600 python tools/wave_parts.py fused 0 $O/wave_parts.jsonl > $O/wp.log 2>&1
+V=$PWD/scratch/variants
+B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e"
+for rep in 1 2; do
+  timeout 600 $B > $O/new_$rep.json 2>>$O/err.log
+  METLDPC_LIB=$V/wave5/libmetldpc.so timeout 600 $B > $O/old_$rep.json 2>>$O/err.log
+done
+for t in 1 4; do METLDPC_REFILL_MIN=$t timeout 600 $B > $O/new_t$t.json 2>>$O/err.log; done
