@@ -460,3 +460,44 @@ def test_syndrome_kernel(c1):
         ref = pack_bits(bp.syndrome(code, unpack_bits(bits[i], code.n)))
         assert np.array_equal(s2[i], ref)
         assert bool(conv[i]) == np.array_equal(s2[i], fr["synd"][i])
+
+
+def _hub_code(D=512):
+    """VN 0 of degree D (the N3 limit, kMaxVnDeg = 512) on D checks (3,0): VN 0 + a cycle of degree-2 VNs."""
+    h = np.zeros((D, D + 1), np.uint8)
+    for j in range(D):
+        h[j, [0, 1 + j, 1 + (j + 1) % D]] = 1
+    return from_dense(h)
+
+
+@pytest.mark.parametrize("rule", RULES)
+def test_pair_accumulator_extremes(rule):
+    """64-bit pair accumulators (N3): VN 0 sums 512 saturated messages (|sum| 2.01e9 of
+    the 2^31 range) with opposite signs in lanes t and t + 32, so the low word's carry into the
+    high word is maximal; L and r of both halves bit-exact against M3 every iteration."""
+    code = _hub_code()
+    hd = B.Code(code)
+    rng = np.random.default_rng(64)
+    n = code.n
+    llr = rng.normal(0.0, 3.0, (64, n)).astype(np.float32)
+    llr[:16, 1:] = 60.0                       # lanes 0-15: every check sends VN 0 about +30
+    llr[32:48, 1:] = 60.0
+    llr[32:48, 1::2] = -60.0                  # lanes 32-47: alternating partner signs -> about -30
+    llr[:16, 0] = 5.0
+    llr[32:48, 0] = -5.0
+    llr[16:32:2, 1:] = -60.0                  # lanes 16, 18, ...: negative partners
+    synd = np.zeros((64, (code.m + 31) // 32), np.uint32)
+    synd[48:] = np.stack([pack_bits(rng.integers(0, 2, code.m)) for _ in range(16)])
+    lanes = (0, 7, 15, 16, 17, 32, 39, 47, 48, 63)
+    N = 3
+    traces = {i: bp.decode(code, llr[i], synd[i], N, early_term=False, rule=rule, prec=32, trace=True) for i in lanes}
+    dec = B.Decoder(hd, 64, rule=rule, max_iter=N, early_term=False)
+    L_t = torch.from_numpy(llr).cuda()
+    S_t = torch.from_numpy(synd.view(np.int32)).cuda()
+    for l in range(1, N + 1):
+        dec.decode(L_t, S_t, max_iter=l)
+        for i in lanes:
+            r, L = dec.dump(i)
+            assert np.array_equal(r.view(np.uint32), traces[i]["r_trace"][l - 1].view(np.uint32)), (l, i)
+            assert np.array_equal(L.view(np.uint32), traces[i]["L_trace"][l - 1].view(np.uint32)), (l, i)
+    assert abs(traces[0]["L_trace"][0][0]) > 15000 and abs(traces[32]["L_trace"][0][0]) > 15000
