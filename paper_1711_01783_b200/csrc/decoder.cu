@@ -707,6 +707,15 @@ metldpc_status metldpc_decoder_create(metldpc_code code, int32_t max_batch, cons
         }
         cudaMemset(w.d1bits, 0, 2 * size_t(L.n_1) * C * sizeof(uint32_t));
         cudaMemset(w.ctl, 0, 32 * sizeof(uint32_t));
+        // Lanes without a frame are computed too (unpredicated CN kernels).  Their lam1 entries
+        // are the degree-1 inputs p of checks with D <= 5, whose output phi is evaluated without an
+        // upper clamp on the premise p <= phi(2^-44) (k_cn_ring / k_cn_pipe / k_cn_tile): a lane that
+        // has not yet held a frame in the streaming decode must therefore read a valid prior, not
+        // whatever a previous allocation left (+0 is one: phi form of |lambda| = +inf).  L and
+        // lambda_a are cleared for the same lanes' determinism.
+        cudaMemset(w.lam1, 0, size_t((L.n_1 + 15) & ~7) * B * sizeof(float));
+        cudaMemset(w.L, 0, 2 * size_t(L.n_a) * B * sizeof(float));
+        cudaMemset(w.lam_a, 0, size_t(L.n_a) * B * sizeof(float));
     }
     // Persisting-L2 window over the workspace's L / accumulator rows (the CN gathers and
     // atomics hit them ~23 times per iteration per VN).  Measured (round 1, C3): +2 % with one

@@ -12,6 +12,7 @@
 Inputs are seeded synthetic frames from synth/ (never from the CUDA path).
 """
 from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -332,3 +333,71 @@ def test_headline_config_sampled_frames():
     for i, o in zip(sample, res):
         assert it[i] == o["iters"] and bool(cv[i]) == o["converged"], (i, it[i], o["iters"])
         assert np.array_equal(unpack_bits(bits[i], code.n), o["bits"]), i
+
+
+# ----------------------------------------------------------------------------- A/B kernel alternatives
+
+_ALT_SCRIPT = r"""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, sys.argv[1])
+from oracle import bp
+from paper_1711_01783_b200 import binding as B
+from synth.codes import make_met_code, random_code
+from synth.frames import gen_batch, unpack_bits
+for code in (make_met_code("r0.1", 2048), random_code(600, 240, np.random.default_rng(11), frac_deg1=0.3, act_deg=(2, 5))):
+    h = B.Code(code)
+    fr = gen_batch(code, 0.3, 5, range(40))
+    llr = np.stack([bp.llr_from_md_f32(fr["v"][i], fr["xnorm"][i], 0.3) for i in range(40)])
+    for rule in (B.RULE_EXACT, B.RULE_PHI_LUT):
+        for msg in (32, 16):
+            dec = B.Decoder(h, 40, rule=rule, max_iter=30, msg_bits=msg)
+            bits, it, cv = dec.decode(torch.from_numpy(llr).cuda(), torch.from_numpy(fr["synd"].view(np.int32)).cuda())
+            torch.cuda.synchronize()
+            bits = bits.cpu().numpy().view(np.uint32)
+            for i in (0, 7, 33, 39):
+                o = bp.decode(code, llr[i], fr["synd"][i], 30, rule=rule, prec=32, msg16=(msg == 16))
+                assert it[i].item() == o["iters"] and bool(cv[i].item()) == o["converged"], (code.name, rule, msg, i)
+                assert np.array_equal(unpack_bits(bits[i], code.n), o["bits"]), (code.name, rule, msg, i)
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", ["METLDPC_RING=0", "METLDPC_RING_CORE=0", "METLDPC_PIPE=0"])
+def test_alternative_kernel_paths(env):
+    """The A/B alternatives kept in the library (per-warp pipeline k_cn_pipe, register-only k_cn_tile
+    for the core or for all exact classes) decode bit-exactly like M3: a subprocess per switch, since
+    the switches are read once per process."""
+    import os
+    import subprocess
+    import sys
+    root = str(Path(__file__).resolve().parents[1])
+    k, v = env.split("=")
+    r = subprocess.run([sys.executable, "-c", _ALT_SCRIPT, root], env=dict(os.environ, **{k: v}),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("msg_bits", [32, 16])
+def test_idle_lanes_over_reused_memory(msg_bits):
+    """Lanes that never hold a frame (40 frames in a 64-lane streaming group) are computed too; the
+    decoder clears their degree-1 priors at allocation, so memory left by earlier, destroyed decoders
+    cannot push the checks' unclamped output phi lookups out of the table (this sequence of codes and
+    decoders created and destroyed faulted before the clear)."""
+    code = make_met_code("r0.1", 2048)
+    fr = gen_batch(code, 0.3, 5, range(40))
+    llr = np.stack([bp.llr_from_md_f32(fr["v"][i], fr["xnorm"][i], 0.3) for i in range(40)])
+    refs = {i: bp.decode(code, llr[i], fr["synd"][i], 30, prec=32, msg16=(msg_bits == 16)) for i in (0, 13, 39)}
+    L_t, S_t = torch.from_numpy(llr).cuda(), torch.from_numpy(fr["synd"].view(np.int32)).cuda()
+    h = dec = None
+    for rep in range(6):   # each code / decoder is created before its predecessor is destroyed
+        h = B.Code(code)
+        for rule in (B.RULE_EXACT, B.RULE_PHI_LUT):
+            dec = B.Decoder(h, 40, rule=rule, max_iter=30, msg_bits=msg_bits, lane_refill=True)
+            bits, it, cv = dec.decode(L_t, S_t)
+            torch.cuda.synchronize()
+            if rule == B.RULE_EXACT:
+                bits = bits.cpu().numpy().view(np.uint32)
+                for i, o in refs.items():
+                    assert it[i].item() == o["iters"] and np.array_equal(unpack_bits(bits[i], code.n), o["bits"]), (rep, i)
